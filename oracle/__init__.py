@@ -1,0 +1,29 @@
+"""CPU oracle for the Haar-domain shift + relight hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import or execute anything under ``oracle/``.  The product path
+(``paper_1705_07272_b200``) never imports it, and the oracle imports nothing from the product:
+the two share no code; only ``synth`` (seeded input generators, none of the method's arithmetic)
+serves both.
+
+What it computes (DESIGN.md §2 lists every reading of the paper):
+
+* ``haar``:   unit-square orthonormal 2D non-separable (quadtree) Haar and unit-interval 1D Haar,
+  forward and inverse, HAAR1 packing.
+* ``shift``:  the shifted pyramid by the paper's own ground-truth procedure (PAPER.md P:535:
+  "rotating it in the spatial domain to generate the ground truth"): inverse transform, pixel
+  shift by box projection ("linear shift"), forward transform.
+* ``relight``: the double product R = T . L'  (PAPER.md eq:tripleSum P:265-266 with the Tripling
+  Coefficient Theorem's scaling case P:287: C_{i j 0} = delta_ij) and the per-vertex
+  fused form r_v = <S_{s_v} L, T_v>.
+
+Everything is fp64 NumPy, written step by step with no blocking, fusion or reordering.
+Pins (tests/test_oracle_*.py, "-m 'not gpu'"): SPEC worked examples, dense
+basis-matrix brute force built from the basis definition, exact ``fractions.Fraction`` overlap
+integrals <psi_i, T_s psi_j> for 1D N=8 and 2D 4x4, closed forms (identity at 0 and N, integer
+composition, DC invariance, Parseval, linearity in the fractional part), SURVEY App. B examples.
+No function here is "parity unpinned".
+"""
+from . import haar, shift, relight  # noqa: F401
+
+__all__ = ["haar", "shift", "relight"]

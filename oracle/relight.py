@@ -1,0 +1,49 @@
+"""Oracle: relight = light-transport inner product, fp64 NumPy -- TEST INFRASTRUCTURE ONLY (see
+oracle/__init__.py; the product path never imports this).
+
+PAPER.md eq:tripleSum writes outgoing radiance as sum_ijk C_ijk a_i b_j c_k with
+C_ijk the integral of three basis functions.  With the transfer vector T holding BRDF x
+visibility projected together (PRT transfer; reading R15) the third factor is
+the constant 1 = the level-0 scaling function, and the Tripling Coefficient Theorem's cases (a)
+and (c) give C_{i j 0} = delta_ij in the orthonormal unit-square basis: the
+triple sum collapses to the plain coefficient dot product  r = sum_k L_k T_k  ("the rotated data
+is plugged in the triple integral computation").
+
+* ``relight``:          R[v][b] = sum_f sum_{k<K_face} T[v][f K_face + k] L'[b][f][k]
+* ``relight_shifted``:  r_v = < S_{s_v} L , T_v >, the shifted pyramid built per vertex by
+                        inverse -> shift -> forward (shift.py); the inverse is shared.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import haar, shift
+
+__all__ = ["relight", "relight_shifted"]
+
+
+def relight(transfer: np.ndarray, light: np.ndarray, faces: int, k_face: int) -> np.ndarray:
+    """transfer [V][faces*k_face], light [B][faces][>= k_face] -> radiance [V][B] (fp64 BLAS)."""
+    T = np.asarray(transfer, dtype=np.float64)
+    L = np.asarray(light, dtype=np.float64)
+    B = L.shape[0]
+    band = L[:, :faces, :k_face].reshape(B, faces * k_face)
+    return T @ band.T
+
+
+def relight_shifted(transfer: np.ndarray, light: np.ndarray, vertex_shifts: np.ndarray) -> np.ndarray:
+    """transfer [V][faces*N*N], light [faces][N*N] (one full pyramid per face), vertex_shifts
+    [V][2] (sy, sx), the same shift for every face of a vertex -> radiance [V] (fp64)."""
+    T = np.asarray(transfer, dtype=np.float64)
+    L = np.asarray(light, dtype=np.float64)
+    F, K = L.shape
+    pixels = [haar.inverse2d(L[f]) for f in range(F)]          # inverse once (shared by vertices)
+    out = np.empty(T.shape[0], dtype=np.float64)
+    for v in range(T.shape[0]):
+        sy, sx = float(vertex_shifts[v][0]), float(vertex_shifts[v][1])
+        acc = 0.0
+        for f in range(F):
+            shifted = haar.forward2d(shift.shift_pixels2d(pixels[f], sy, sx))
+            acc += float(np.dot(shifted, T[v, f * K:(f + 1) * K]))
+        out[v] = acc
+    return out
