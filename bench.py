@@ -1,0 +1,364 @@
+"""Benchmark of the hot path (BASELINE.json metric): relit vertices/s (and shifted Haar coefficients
+/s) on config c5 -- 6 x 256 x 256 cube-map light, 64 light/rotation frames, 1M vertices with
+6 x 1024-coefficient transfer vectors -- as a fraction of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
+
+One step = the whole hot path over one batch:
+  (a0-a5) haar_shift_coeffs: 64 frames x 6 faces of 256x256 Haar pyramids shifted in the Haar
+          domain (rank 0; N=1: full pyramids written, the relight reads their band in place;
+          N>1: band written, then NCCL-broadcast);
+  (a6)    relight_vertices: R[v][b] = <T_v, L'_b band> for this rank's vertex rows;
+  (e)     N>1: radiance gathered to rank 0 in chunks overlapped with the relight.
+Inputs are resident in HBM when timing starts; T (24.6 GB) is streamed every step, so the working
+set is far larger than L2 (no flush needed).  Rank 0 prints ONE JSON line.
+
+--impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on this host's cores on
+a bounded sample of the same workload (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "relit_vertices_per_sec"
+UNIT = "vertices/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0     # GB/s, B200_PROFILING.md fallback
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c5")
+    p.add_argument("--vertices", type=int, default=None, help="override V (debug only)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--chunks", type=int, default=4)
+    return p.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 100 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active", "--format=csv,noheader,nounits",
+               "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                mask = int(r[2], 16) if r[2].startswith("0x") else int(r[2])
+                for bit, name in REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        reasons.add(name)
+            except ValueError:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ oracle arm
+
+def oracle_sample(cfg, frames_sample=1, rows_sample=4000, seed_off=0):
+    """Time the fp64 oracle on a bounded sample of the step; returns (seconds for the FULL step,
+    extrapolated linearly from the sample, sample description, threads)."""
+    from oracle import relight as orelight
+    from oracle import shift as oshift
+    N = 1 << cfg.log2n
+    light = synth.light_pyramids(cfg.seed, frames_sample, cfg.faces, cfg.log2n)
+    s = synth.c5_shifts(cfg.seed, cfg.frames, cfg.log2n)[:frames_sample]
+    sh = np.broadcast_to(s[:, None, :], (frames_sample, cfg.faces, 2))
+    t0 = time.perf_counter()
+    shifted = oshift.shift_coeffs(light, sh, 2)
+    t_shift = time.perf_counter() - t0
+    T = synth.transfer_rows(cfg.seed, seed_off, rows_sample, cfg.faces, cfg.k_face)
+    Lb = np.concatenate([shifted] * (cfg.frames // frames_sample + 1))[: cfg.frames]
+    t0 = time.perf_counter()
+    orelight.relight(T, Lb, cfg.faces, cfg.k_face)
+    t_rel = time.perf_counter() - t0
+    full = t_shift * (cfg.frames / frames_sample) + t_rel * (cfg.vertices / rows_sample)
+    desc = (f"oracle fp64: shift of {frames_sample}/{cfg.frames} frames x {cfg.faces} faces of {N}x{N} "
+            f"({t_shift:.3f}s) + relight of {rows_sample}/{cfg.vertices} vertex rows x {cfg.frames} frames "
+            f"({t_rel:.3f}s); step time extrapolated linearly to the full workload")
+    return full, desc
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        blas = [i for i in info if i.get("user_api") == "blas"]
+        if blas:
+            return int(blas[0].get("num_threads", 1))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    V = cfg.vertices
+    warm, steps = max(args.warmup, 0), max(args.steps, 1)
+    times = []
+    for i in range(warm + steps):
+        full, desc = oracle_sample(cfg, 1, 2000, seed_off=i * 2000)
+        if i >= warm:
+            times.append(full)
+    t = statistics.median(times)
+    value = V / t
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, gpus):
+    N = 1 << cfg.log2n
+    return {"workload": f"{cfg.name}: {cfg.faces}x{N}x{N} cube-map light, {cfg.frames} frames, "
+                        f"{cfg.vertices} vertices, transfer {cfg.faces}x{cfg.k_face} coefficients",
+            "faces": cfg.faces, "N": N, "frames": cfg.frames, "vertices": cfg.vertices, "k_face": cfg.k_face,
+            "parallelism": f"dp{gpus} over vertex rows", "l2": "no flush: transfer matrix streamed every step "
+            f"({cfg.vertices * cfg.faces * cfg.k_face * 4 / 1e9:.1f} GB) >> 126 MB L2"}
+
+
+# ------------------------------------------------------------------------------------ our arm
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_07272_b200 as hs
+    from paper_1705_07272_b200 import dist as hsdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    V = args.vertices or cfg.vertices
+    n, F, B, kf = cfg.log2n, cfg.faces, cfg.frames, cfg.k_face
+    N = 1 << n
+    K = F * kf
+    r0, rows = hsdist.shard_rows(V, world, rank)
+
+    # ---- inputs resident in HBM (untimed)
+    T = torch.empty((rows, K), dtype=torch.float32, device=dev)
+    hs.hs_fill_transfer(T, r0, F, kf, cfg.seed, synth.STREAM_T)
+    light_np = synth.light_pyramids(cfg.seed, B, F, n)
+    shifts = np.broadcast_to(synth.c5_shifts(cfg.seed, B, n)[:, None, :], (B, F, 2)).copy()
+    light = torch.from_numpy(light_np).to(dev)
+    full_out = world == 1
+    shifted = torch.empty((B, F, N * N if full_out else kf), dtype=torch.float32, device=dev)
+    ws = torch.empty(hs.haar_shift_workspace_bytes(2, n, F, B), dtype=torch.uint8, device=dev)
+    R = torch.empty((rows, B), dtype=torch.float32, device=dev)
+    R_full = torch.empty((V, B), dtype=torch.float32, device=dev) if (rank == 0 and world > 1) else None
+    stream = torch.cuda.current_stream()
+    launches = {"n": 0}
+    rel_events = []
+
+    def relight_fn(Tc, band, Rc):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hs.relight_vertices(Tc, band, F, kf, out=Rc)
+        e1.record(stream)
+        launches["n"] += hs.last_launch_count()
+        rel_events.append((e0, e1, Tc.shape[0]))
+
+    def step():
+        """One pass of the hot path; returns this rank's result tensor (R, or R_full on rank 0)."""
+        if rank == 0:
+            hs.haar_shift_coeffs(light, shifts, 2, n if full_out else cfg.band_levels, out=shifted, workspace=ws)
+            launches["n"] += hs.last_launch_count()
+        if world > 1:
+            hsdist.broadcast_band(shifted)
+            _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
+            return full
+        relight_fn(T, shifted, R)
+        return R
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches["n"] = 0
+    rel_events.clear()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    rel_ms = [a.elapsed_time(b) for a, b, _ in rel_events]
+    rel_rows = [r for _, _, r in rel_events]
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    gpu_launches = launches["n"]
+
+    # ---- dominant kernel roofline (relight): algorithmic bytes per launch / average launch time
+    peak, peak_src = hbm_peak()
+    bytes_per_row = K * 4 + B * 4
+    alg_bytes = [r * bytes_per_row + B * K * 4 for r in rel_rows]
+    avg_ms = sum(rel_ms) / len(rel_ms)
+    achieved = (sum(alg_bytes) / len(alg_bytes)) / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{cfg.name}:relight_b{B}")
+    except Exception:
+        pass
+
+    # ---- end to end through the public API with host buffers (pinned), N GPUs
+    e2e = None
+    if not args.no_e2e:
+        light_h = torch.from_numpy(light_np).pin_memory()
+        out_rows = V if rank == 0 else 0
+        Rh = torch.empty((out_rows, B), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            if rank == 0:
+                light.copy_(light_h, non_blocking=True)
+            res = step()
+            if res is not None and rank == 0:
+                Rh.copy_(res, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": V / (float(e_ms.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(light_np.nbytes) if rank == 0 else 0,
+               "d2h_bytes_per_step": int(out_rows * B * 4),
+               "note": "per step: pinned H2D of the 64 light pyramids + shift + relight (+ gather) + D2H of "
+                       "the full radiance on rank 0; T is scene data resident in HBM"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": V / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(cfg, world),
+            "vertex_frames_per_sec": V * B / (ms_max * 1e-3),
+            "shift_coeffs_per_sec": B * F * N * N / (ms_max * 1e-3),
+            "roofline": {"bound": "hbm", "kernel": "relight_vertices", "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes),
+                         "avg_launch_ms": avg_ms, "share_of_step": sum(rel_ms) / args.steps / ms},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            full, desc = oracle_sample(cfg, 1, 4000)
+            line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                                    "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    cfg = synth.config(args.config)
+    if args.vertices:
+        cfg = synth.Config(**{**cfg.__dict__, "vertices": args.vertices})
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

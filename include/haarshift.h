@@ -1,0 +1,158 @@
+/* haarshift.h -- C ABI of the B200-native Haar-domain shift + relight hot path.
+ *
+ * Method: Alnasser & Foroosh, "Non-Linear Phase-Shifting of Haar Wavelets for Run-Time
+ * All-Frequency Lighting" (arXiv 1705.07272), /root/reference/PAPER.md cited as P:<line>.
+ * Conventions and every reading of the paper: DESIGN.md §2, §4.
+ *
+ * Data conventions (all entry points)
+ *   - A 2D face of side N = 2^log2n holds N*N fp32 unit-square orthonormal Haar coefficients in
+ *     HAAR1 order: index 0 = scaling; level l (0 <= l < log2n), type t (H=0, V=1,
+ *     D=2), cell (i, j) at 4^l*(1+t) + i*2^l + j.  Wavelet signs: H + left half,
+ *     V + top half, D + main diagonal.  Rows = theta (top first), columns = phi.
+ *   - A 1D signal of length N holds N fp32 unit-interval Haar coefficients: index 0 = scaling,
+ *     level l cell k at 2^l + k.
+ *   - Every face is an independent N x N periodic signal (cube faces are compressed separately,
+ *     P:306-312; R3).
+ *   - A shift s (finest-pixel units) maps f'(x) = f(x - s) followed by the box projection onto
+ *     the same pixels (R4, R5): content moves to higher indices; shifts are (sy, sx).
+ *
+ * Memory and ownership
+ *   - Unless stated otherwise pointers are CUDA DEVICE pointers owned by the caller; the library
+ *     keeps no pointer after return.  Work is enqueued on `stream` (cudaStream_t passed as
+ *     void*; NULL = legacy default stream) and returns without synchronising; buffers must stay
+ *     valid until the stream work completes.
+ *   - All device pointers must be 16-byte aligned (HS_ERR_ALIGNMENT otherwise).
+ *   - Stateless and re-entrant; safe to call concurrently from several host threads on
+ *     different streams with distinct workspaces.  Capturable into a CUDA graph.
+ *
+ * Errors
+ *   - Every entry point validates all arguments BEFORE enqueuing any work and returns a status.
+ *     No exceptions cross the ABI, nothing calls exit(), there is no CPU fallback and no other
+ *     backend: on a device that is not sm_100 the call fails with HS_ERR_UNSUPPORTED.
+ *   - HS_ERR_CUDA: a CUDA runtime error at launch; hs_last_cuda_error() returns the detail string
+ *     (thread-local, valid until the next call on the same thread).
+ */
+#ifndef HAARSHIFT_H_
+#define HAARSHIFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HS_API __attribute__((visibility("default")))
+#else
+#define HS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HS_OK = 0,
+  HS_ERR_INVALID_ARG = 1,  /* null pointer, size out of range, non-finite shift, in == out ... */
+  HS_ERR_ALIGNMENT = 2,    /* a device pointer is not 16-byte aligned                         */
+  HS_ERR_UNSUPPORTED = 3,  /* device is not sm_100 (B200), or a shape this build does not cover */
+  HS_ERR_CUDA = 4          /* CUDA runtime error; see hs_last_cuda_error()                     */
+} hs_status;
+
+#define HS_MAX_LOG2N 12
+
+/* ---------------------------------------------------------------------------------------------
+ * haar_shift_coeffs -- shift of Haar coefficient pyramids computed directly in the Haar domain
+ * (SURVEY.md §8(a) rows a0-a5).
+ *
+ * Defines:  P:459 ("a rotation with respect to the azimuth angle ... becomes a linear shift"),
+ *           P:503-508 (all rotations = rotation about the theta-axis + "a simple shifting along
+ *           the phi-axis"), P:331/P:408/P:463 (coefficients are finite differences), eq:pde1-2
+ *           P:416-425 with identity Jacobian (the difference fields translate), eq:conv/eq:tker/
+ *           eq:sker P:466-478 and P:486-497 (recursive [1,1] x [1,2,1] synthesis, O(N))
+ *           (start at a coarser level: exact here for dyadic shifts).  No inverse transform.
+ *
+ *   in, out       [batch][faces][K] fp32, K = N*N (ndim = 2) or N (ndim = 1), HAAR1 order.
+ *                 out must not overlap in.  With band_levels < log2n, out is
+ *                 [batch][faces][Kb] with Kb = 4^band_levels (2D) or 2^band_levels (1D): the
+ *                 HAAR1 prefix holding the scaling coefficient and levels < band_levels.
+ *   ndim          1 or 2.
+ *   log2n         1 .. HS_MAX_LOG2N (N = 2^log2n).
+ *   faces, batch  >= 1.
+ *   shifts_host   HOST pointer, [batch][faces][ndim] fp64, (sy, sx) order in 2D, any finite real
+ *                 value (reduced mod N internally in fp64).
+ *   band_levels   0 .. log2n (log2n = full pyramid).
+ *   workspace     device scratch of at least haar_shift_workspace_bytes(...) bytes (may be NULL
+ *                 when that size is 0).  Contents on entry are irrelevant.
+ * Result: out = S_s in, equal (to fp32 rounding) to forward(box_shift(inverse(in))).
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, int faces,
+                            int batch, const double* shifts_host, int band_levels,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t haar_shift_workspace_bytes(int ndim, int log2n, int faces, int batch);
+
+/* ---------------------------------------------------------------------------------------------
+ * relight_vertices -- per-vertex light-transport inner product.
+ *
+ * Defines:  eq:tripleSum P:253-266 with the Tripling Coefficient Theorem's scaling case
+ *           (P:287): with the transfer vector holding BRDF x visibility (PRT transfer,
+ *           P:213-222) the triple sum is the coefficient dot product; "the rotated data is
+ *           plugged in the triple integral computation".
+ *
+ *   radiance[v][b] = sum_{f < faces} sum_{k < k_face} transfer[v][f*k_face + k]
+ *                                                     * light[b][f][k]   (light row stride below)
+ *   transfer      [num_vertices][faces*k_face] fp32 row-major (64-bit indexing).
+ *   light         [batch][faces][light_face_stride] fp32; only the first k_face entries of each
+ *                 face are read, so a full shifted pyramid (stride N*N) or a band (stride k_face)
+ *                 can be passed.  light_face_stride >= k_face and a multiple of 4.
+ *   k_face        a power of 4 (the HAAR1 prefix 4^k: scaling + levels < k), >= 4.
+ *   batch         1 .. 1024 light/rotation frames.
+ *   radiance      [num_vertices][batch] fp32.
+ * Accumulation is fp32 (batch <= 8: CUDA-core streaming GEMV; batch multiple of 64: tcgen05
+ * split-precision GEMM with fp32-level accuracy; other batches: CUDA-core tiled GEMM).
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
+                           const float* light, int64_t light_face_stride, int batch,
+                           float* radiance, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * relight_vertices_shifted -- fused per-vertex shift + relight:
+ *   radiance[v] = < S_{shift_v} L , T_v >, the shift applied identically to every face.
+ *
+ * Defines:  P:513 (per pixel, coefficients rotated by the normal's azimuth and elevation),
+ *           P:514 (coarser levels by the recursive h_s / h_t filters).
+ *
+ *   transfer       [num_vertices][faces*N*N] fp32 (full pyramids per face, 64-bit indexing).
+ *   light          [faces][N*N] fp32, one pyramid per face.
+ *   vertex_shifts  DEVICE pointer [num_vertices][2] fp32 (sy, sx), finite.
+ *   radiance       [num_vertices] fp32.
+ *   workspace      >= relight_shifted_workspace_bytes(...) bytes.
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, int faces,
+                                   const float* light, int log2n, const float* vertex_shifts,
+                                   float* radiance, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+HS_API size_t relight_shifted_workspace_bytes(int64_t num_vertices, int faces, int log2n);
+
+/* ---------------------------------------------------------------------------------------------
+ * hs_fill_transfer -- seeded synthetic transfer rows, generated in place (input generator, not
+ * part of the method; bit-identical to synth.transfer_rows):
+ *   T[v][f*k_face + k] = u * 2^-level(k), u = ((h >> 40) - 2^23) / 2^23,
+ *   h = splitmix64(splitmix64(seed + stream * 0xD1B54A32D192ED03) + global_index),
+ *   global_index = (row_start + v) * faces * k_face + f * k_face + k; k == 0 entries are |u|.
+ *   out [row_count][faces*k_face] device fp32.
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status hs_fill_transfer(float* out, int64_t row_start, int64_t row_count, int faces,
+                           int k_face, uint64_t seed, uint64_t stream_id, void* stream);
+
+/* Kernel-launch count of the most recent successful call on this thread (for bench accounting). */
+HS_API int hs_last_launch_count(void);
+
+HS_API const char* hs_status_string(hs_status s);
+HS_API const char* hs_last_cuda_error(void);
+/* ABI version, bumped on any signature change. */
+HS_API int hs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAARSHIFT_H_ */

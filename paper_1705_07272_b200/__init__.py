@@ -1,0 +1,32 @@
+"""B200-native Haar-domain shift + relight (Alnasser & Foroosh, arXiv 1705.07272).
+
+Thin Python binding over the C ABI of libhaarshift.so (include/haarshift.h): argument marshalling
+only -- every step of the hot path runs in the library's sm_100a CUDA kernels.  PyTorch provides
+device memory and streams.  Function names follow the C ABI:
+
+* ``haar_shift_coeffs``        shifted Haar pyramids, computed in the Haar domain
+* ``relight_vertices``         per-vertex transfer inner products (a6)
+* ``relight_vertices_shifted`` fused per-vertex shift + relight (a7)
+* ``hs_fill_transfer``         seeded synthetic transfer rows generated in place (input generator)
+
+See DESIGN.md for the method, its readings of the paper, layouts and kernels.
+"""
+from __future__ import annotations
+
+from ._lib import HaarShiftError, load  # noqa: F401
+from .api import (  # noqa: F401
+    haar_shift_coeffs,
+    haar_shift_workspace_bytes,
+    hs_fill_transfer,
+    last_launch_count,
+    relight_shifted_workspace_bytes,
+    relight_vertices,
+    relight_vertices_shifted,
+    shift_and_relight,
+)
+
+__all__ = [
+    "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_workspace_bytes", "hs_fill_transfer",
+    "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_vertices_shifted",
+    "shift_and_relight",
+]

@@ -1,0 +1,145 @@
+"""Python binding of the C ABI (include/haarshift.h): marshalling of torch tensors to pointers,
+nothing else.  All tensors passed as device arguments must be CUDA float32, contiguous and 16-byte
+aligned; results are new tensors unless ``out=`` is given.  Work is enqueued on the current torch
+CUDA stream (or ``stream=``)."""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from ._lib import check, load
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def last_launch_count() -> int:
+    """Kernel launches enqueued by the most recent C-ABI call on this thread."""
+    return int(load().hs_last_launch_count())
+
+
+def haar_shift_workspace_bytes(ndim: int, log2n: int, faces: int, batch: int) -> int:
+    return int(load().haar_shift_workspace_bytes(ndim, log2n, faces, batch))
+
+
+def relight_shifted_workspace_bytes(num_vertices: int, faces: int, log2n: int) -> int:
+    return int(load().relight_shifted_workspace_bytes(num_vertices, faces, log2n))
+
+
+def haar_shift_coeffs(coeffs: torch.Tensor, shifts, ndim: int = 2, band_levels: Optional[int] = None,
+                      out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """coeffs [batch][faces][K] (K = N*N in 2D, N in 1D) -> shifted pyramids [batch][faces][Kb].
+
+    shifts: host array-like [batch][faces][ndim] (fp64; (sy, sx) in 2D)."""
+    lib = load()
+    _dev_f32(coeffs, "coeffs")
+    if coeffs.dim() != 3:
+        raise ValueError("coeffs must be [batch][faces][K]")
+    B, F, K = coeffs.shape
+    n = int(K).bit_length() - 1
+    if ndim == 2:
+        if n % 2 or (1 << n) != K:
+            raise ValueError("2D faces must hold 4**log2n coefficients")
+        log2n = n // 2
+    else:
+        if (1 << n) != K:
+            raise ValueError("1D signals must hold 2**log2n coefficients")
+        log2n = n
+    band = log2n if band_levels is None else int(band_levels)
+    kb = (4 if ndim == 2 else 2) ** band
+    sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(B, F, ndim))
+    if out is None:
+        out = torch.empty((B, F, kb), dtype=torch.float32, device=coeffs.device)
+    _dev_f32(out, "out")
+    need = haar_shift_workspace_bytes(ndim, log2n, F, B)
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
+    ws_ptr = workspace.data_ptr() if (need and workspace is not None) else None
+    st = lib.haar_shift_coeffs(coeffs.data_ptr(), out.data_ptr(), ndim, log2n, F, B,
+                               sh.ctypes.data_as(ctypes.c_void_p), band, ws_ptr, need, _stream_ptr(stream))
+    check("haar_shift_coeffs", st)
+    return out
+
+
+def relight_vertices(transfer: torch.Tensor, light: torch.Tensor, faces: int, k_face: int,
+                     out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """transfer [V][faces*k_face], light [batch][faces][stride >= k_face] -> radiance [V][batch]."""
+    lib = load()
+    _dev_f32(transfer, "transfer")
+    _dev_f32(light, "light")
+    V = transfer.shape[0]
+    if transfer.numel() != V * faces * k_face:
+        raise ValueError("transfer must be [V][faces*k_face]")
+    if light.dim() != 3 or light.shape[1] != faces:
+        raise ValueError("light must be [batch][faces][stride]")
+    B, _, stride = light.shape
+    if out is None:
+        out = torch.empty((V, B), dtype=torch.float32, device=transfer.device)
+    _dev_f32(out, "out")
+    st = lib.relight_vertices(transfer.data_ptr(), V, faces, k_face, light.data_ptr(), stride, B, out.data_ptr(),
+                              _stream_ptr(stream))
+    check("relight_vertices", st)
+    return out
+
+
+def relight_vertices_shifted(transfer: torch.Tensor, light: torch.Tensor, vertex_shifts: torch.Tensor,
+                             out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """transfer [V][faces*N*N], light [faces][N*N], vertex_shifts [V][2] (device fp32) -> [V]."""
+    lib = load()
+    _dev_f32(transfer, "transfer")
+    _dev_f32(light, "light")
+    _dev_f32(vertex_shifts, "vertex_shifts")
+    F, K = light.shape
+    n = (int(K).bit_length() - 1) // 2
+    V = transfer.shape[0]
+    if transfer.numel() != V * F * K or vertex_shifts.shape != (V, 2):
+        raise ValueError("shape mismatch")
+    if out is None:
+        out = torch.empty((V,), dtype=torch.float32, device=transfer.device)
+    need = relight_shifted_workspace_bytes(V, F, n)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=transfer.device)
+    st = lib.relight_vertices_shifted(transfer.data_ptr(), V, F, light.data_ptr(), n, vertex_shifts.data_ptr(),
+                                      out.data_ptr(), workspace.data_ptr(), need, _stream_ptr(stream))
+    check("relight_vertices_shifted", st)
+    return out
+
+
+def hs_fill_transfer(out: torch.Tensor, row_start: int, faces: int, k_face: int, seed: int, stream_id: int,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Fill out [rows][faces*k_face] with the seeded synthetic transfer rows (synth.transfer_rows)."""
+    lib = load()
+    _dev_f32(out, "out")
+    rows = out.shape[0]
+    st = lib.hs_fill_transfer(out.data_ptr(), row_start, rows, faces, k_face, seed % 2**64, stream_id % 2**64,
+                              _stream_ptr(stream))
+    check("hs_fill_transfer", st)
+    return out
+
+
+def shift_and_relight(light: torch.Tensor, shifts, transfer: torch.Tensor, faces: int, k_face: int,
+                      band_levels: int, shifted: Optional[torch.Tensor] = None, radiance: Optional[torch.Tensor] = None,
+                      workspace: Optional[torch.Tensor] = None,
+                      stream: Optional[torch.cuda.Stream] = None):
+    """One step of the hot path: shift every frame's pyramids in the Haar domain (band only), then
+    relight every vertex with the shifted band.  Returns (shifted band, radiance)."""
+    shifted = haar_shift_coeffs(light, shifts, 2, band_levels, out=shifted, workspace=workspace, stream=stream)
+    radiance = relight_vertices(transfer, shifted, faces, k_face, out=radiance, stream=stream)
+    return shifted, radiance

@@ -1,0 +1,196 @@
+// C-ABI entry points (include/haarshift.h): argument validation before any launch, status codes,
+// thread-local error detail.  No CPU fallback, no other backend.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace hs {
+
+thread_local int g_launches = 0;
+namespace {
+thread_local char g_err[512] = "";
+thread_local int g_last_launches = 0;
+std::atomic<int> g_dev_ok[64];  // 0 unknown, 1 sm_100, 2 other
+
+inline bool is_pow4(long long x) {
+  if (x < 1 || (x & (x - 1))) return false;
+  int b = 0;
+  while ((1ll << b) < x) ++b;
+  return (b & 1) == 0;
+}
+inline bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + nb && pb < pa + na;
+}
+constexpr long long kRelightChunk = 128;  // vertices per chunk of the per-vertex shift path
+
+}  // namespace
+
+void set_cuda_error(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+hs_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    set_cuda_error(e, "cudaGetDevice");
+    return HS_ERR_CUDA;
+  }
+  if (dev < 0 || dev >= 64) return HS_ERR_UNSUPPORTED;
+  int st = g_dev_ok[dev].load(std::memory_order_relaxed);
+  if (st == 0) {
+    int major = 0, minor = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) {
+      set_cuda_error(e, "cudaDeviceGetAttribute");
+      return HS_ERR_CUDA;
+    }
+    st = (major == 10 && minor == 0) ? 1 : 2;
+    g_dev_ok[dev].store(st, std::memory_order_relaxed);
+  }
+  if (st != 1) {
+    snprintf(g_err, sizeof(g_err), "device %d is not sm_100 (B200); this library is sm_100a only", dev);
+    return HS_ERR_UNSUPPORTED;
+  }
+  return HS_OK;
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+int hs_abi_version(void) { return 1; }
+
+const char* hs_status_string(hs_status s) {
+  switch (s) {
+    case HS_OK: return "HS_OK";
+    case HS_ERR_INVALID_ARG: return "HS_ERR_INVALID_ARG";
+    case HS_ERR_ALIGNMENT: return "HS_ERR_ALIGNMENT";
+    case HS_ERR_UNSUPPORTED: return "HS_ERR_UNSUPPORTED";
+    case HS_ERR_CUDA: return "HS_ERR_CUDA";
+  }
+  return "HS_ERR_UNKNOWN";
+}
+
+const char* hs_last_cuda_error(void) { return g_err; }
+int hs_last_launch_count(void) { return g_last_launches; }
+
+size_t haar_shift_workspace_bytes(int ndim, int log2n, int faces, int batch) {
+  if ((ndim != 1 && ndim != 2) || log2n < 1 || log2n > HS_MAX_LOG2N || faces < 1 || batch < 1) return 0;
+  return shift_workspace_bytes_impl(ndim, log2n, (long long)faces * batch);
+}
+
+hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, int faces, int batch,
+                            const double* shifts_host, int band_levels, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!in || !out || !shifts_host) return HS_ERR_INVALID_ARG;
+  if (ndim != 1 && ndim != 2) return HS_ERR_INVALID_ARG;
+  if (log2n < 1 || log2n > HS_MAX_LOG2N || faces < 1 || batch < 1) return HS_ERR_INVALID_ARG;
+  if (band_levels < 0 || band_levels > log2n) return HS_ERR_INVALID_ARG;
+  const long long nfaces = (long long)faces * batch;
+  for (long long i = 0; i < nfaces * ndim; ++i)
+    if (!std::isfinite(shifts_host[i])) return HS_ERR_INVALID_ARG;
+  const size_t K = (ndim == 2) ? ((size_t)1 << (2 * log2n)) : ((size_t)1 << log2n);
+  const size_t Kb = (ndim == 2) ? ((size_t)1 << (2 * band_levels)) : ((size_t)1 << band_levels);
+  if (overlap(in, nfaces * K * 4, out, nfaces * Kb * 4)) return HS_ERR_INVALID_ARG;
+  const size_t need = shift_workspace_bytes_impl(ndim, log2n, nfaces);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(in) || !aligned16(out) || (need > 0 && !aligned16(workspace))) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_shift(in, out, ndim, log2n, faces, nfaces, (long long)faces * (long long)K, shifts_host, nullptr,
+                   nullptr, band_levels, workspace, workspace_bytes, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
+                           const float* light, int64_t light_face_stride, int batch, float* radiance,
+                           void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!transfer || !light || !radiance) return HS_ERR_INVALID_ARG;
+  if (num_vertices < 1 || faces < 1 || batch < 1 || batch > 1024) return HS_ERR_INVALID_ARG;
+  if (!is_pow4(k_face) || k_face < 4 || k_face > (1 << (2 * HS_MAX_LOG2N))) return HS_ERR_INVALID_ARG;
+  if (light_face_stride < k_face || (light_face_stride & 3)) return HS_ERR_INVALID_ARG;
+  if ((long long)faces * k_face > (1ll << 30)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance)) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_relight(transfer, num_vertices, faces, k_face, light, light_face_stride, batch, radiance,
+                     (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+size_t relight_shifted_workspace_bytes(int64_t num_vertices, int faces, int log2n) {
+  if (num_vertices < 1 || faces < 1 || log2n < 1 || log2n > HS_MAX_LOG2N) return 0;
+  const long long vc = num_vertices < kRelightChunk ? num_vertices : kRelightChunk;
+  const long long nf = vc * faces;
+  const size_t shift_ws = shift_workspace_bytes_impl(2, log2n, nf);
+  const size_t fp = ((size_t)nf * sizeof(FaceParam) + 255) & ~(size_t)255;
+  const size_t pyr = (size_t)nf * ((size_t)1 << (2 * log2n)) * sizeof(float);
+  return shift_ws + fp + pyr;
+}
+
+hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, int faces, const float* light,
+                                   int log2n, const float* vertex_shifts, float* radiance, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!transfer || !light || !vertex_shifts || !radiance || !workspace) return HS_ERR_INVALID_ARG;
+  if (num_vertices < 1 || faces < 1 || log2n < 1 || log2n > HS_MAX_LOG2N) return HS_ERR_INVALID_ARG;
+  const size_t need = relight_shifted_workspace_bytes(num_vertices, faces, log2n);
+  if (workspace_bytes < need) return HS_ERR_INVALID_ARG;
+  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance) || !aligned16(workspace) ||
+      (reinterpret_cast<uintptr_t>(vertex_shifts) & 7))
+    return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long vc = num_vertices < kRelightChunk ? num_vertices : kRelightChunk;
+  const long long K = (long long)faces << (2 * log2n);
+  const size_t shift_ws = shift_workspace_bytes_impl(2, log2n, vc * faces);
+  const size_t fpb = ((size_t)vc * faces * sizeof(FaceParam) + 255) & ~(size_t)255;
+  char* base = (char*)workspace;
+  FaceParam* fp = reinterpret_cast<FaceParam*>(base + shift_ws);
+  float* S = reinterpret_cast<float*>(base + shift_ws + fpb);
+  for (long long v0 = 0; v0 < num_vertices; v0 += vc) {
+    const long long nv = (num_vertices - v0) < vc ? (num_vertices - v0) : vc;
+    s = launch_shift(light, S, 2, log2n, faces, nv * faces, 0, nullptr, vertex_shifts + 2 * v0, fp, log2n,
+                     workspace, shift_ws, st);
+    if (s != HS_OK) break;
+    s = launch_rowdot(transfer + v0 * K, S, nv, K, radiance + v0, st);
+    if (s != HS_OK) break;
+  }
+  g_last_launches = g_launches;
+  return s;
+}
+
+hs_status hs_fill_transfer(float* out, int64_t row_start, int64_t row_count, int faces, int k_face,
+                           uint64_t seed, uint64_t stream_id, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!out || row_start < 0 || row_count < 1 || faces < 1) return HS_ERR_INVALID_ARG;
+  if (!is_pow4(k_face)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(out)) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_fill_transfer(out, row_start, row_count, faces, k_face, seed, stream_id, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+}  // extern "C"

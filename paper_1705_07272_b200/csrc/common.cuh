@@ -1,0 +1,150 @@
+// Internal declarations shared by the translation units of libhaarshift.so.
+// Nothing here is visible through the C ABI (include/haarshift.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "haarshift.h"
+
+namespace hs {
+
+// ----------------------------------------------------------------------------------- errors
+
+void set_cuda_error(cudaError_t e, const char* where);
+hs_status check_device();                 // HS_ERR_UNSUPPORTED unless the current device is sm_100
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+extern thread_local int g_launches;       // kernel launches enqueued by the current ABI call
+
+#define HS_CHECK_LAUNCH(where)                                   \
+  do {                                                           \
+    cudaError_t e_ = cudaGetLastError();                         \
+    if (e_ != cudaSuccess) {                                     \
+      ::hs::set_cuda_error(e_, where);                           \
+      return HS_ERR_CUDA;                                        \
+    }                                                            \
+    ++::hs::g_launches;                                          \
+  } while (0)
+
+#define HS_CHECK_CUDA(call, where)                               \
+  do {                                                           \
+    cudaError_t e_ = (call);                                     \
+    if (e_ != cudaSuccess) {                                     \
+      ::hs::set_cuda_error(e_, where);                           \
+      return HS_ERR_CUDA;                                        \
+    }                                                            \
+  } while (0)
+
+// ----------------------------------------------------------------------------------- shift
+
+// Per-face shift parameters, computed in fp64 on the host (or by shift_params_kernel on the
+// device for per-vertex shifts) -- SURVEY.md §8(a) row a0.
+struct FaceParam {
+  int m;         // working level: levels >= m are exact permutations, the recursion runs to m
+  int Qy, Qx;    // integer part of the shift at level m (in level-m cells), in [0, 2^m)
+  int qy, qx;    // integer part of the shift at the finest level n, in [0, N)
+  float wy, wx;  // fractional parts phi (box-projection weights w1 = phi, w0 = 1 - phi)
+};
+
+// fp64 reduction s -> (q, phi): s mod N, q = floor, phi = s - q  (R4/R5).
+__host__ __device__ inline void split_shift(double s, int N, int* q, double* phi) {
+  double r = fmod(s, (double)N);
+  if (r < 0.0) r += (double)N;
+  double fq = floor(r);
+  double p = r - fq;
+  int qi = (int)fq;
+  if (qi >= N) qi -= N;
+  *q = qi;
+  *phi = p;
+}
+
+__host__ __device__ inline int v2_capped(int q, int n) {  // 2-adic valuation, v2(0) = n
+  if (q == 0) return n;
+  int v = 0;
+  while (((q >> v) & 1) == 0 && v < n) ++v;
+  return v;
+}
+
+__host__ __device__ inline FaceParam make_face_param_2d(double sy, double sx, int n) {
+  const int N = 1 << n;
+  int qy, qx;
+  double py, px;
+  split_shift(sy, N, &qy, &py);
+  split_shift(sx, N, &qx, &px);
+  FaceParam fp;
+  if (py == 0.0 && px == 0.0) {
+    int v = v2_capped(qy, n);
+    int vx = v2_capped(qx, n);
+    if (vx < v) v = vx;
+    fp.m = n - v;
+  } else {
+    fp.m = n;
+  }
+  fp.Qy = qy >> (n - fp.m);
+  fp.Qx = qx >> (n - fp.m);
+  fp.qy = qy;
+  fp.qx = qx;
+  fp.wy = (float)py;
+  fp.wx = (float)px;
+  return fp;
+}
+
+__host__ __device__ inline FaceParam make_face_param_1d(double s, int n) {
+  const int N = 1 << n;
+  int q;
+  double p;
+  split_shift(s, N, &q, &p);
+  FaceParam fp;
+  fp.m = (p == 0.0) ? n - v2_capped(q, n) : n;
+  fp.Qy = 0;
+  fp.Qx = q >> (n - fp.m);
+  fp.qy = 0;
+  fp.qx = q;
+  fp.wy = 0.f;
+  fp.wx = (float)p;
+  return fp;
+}
+
+constexpr int kMaxFacesPerLaunch = 512;
+
+struct ShiftArgs {
+  const float* in;            // face g reads in + (g / faces) * in_batch_stride + (g % faces) * K
+  float* out;                 // face g writes out + g * out_face_stride
+  float* ws;                  // per-face coarse fields (see shift_workspace_layout)
+  unsigned* counters;         // per-face tile-completion counters (zeroed before launch)
+  const FaceParam* dev_fp;    // device FaceParams (per-vertex path) or nullptr -> use fp[]
+  long long in_batch_stride;  // elements; 0 broadcasts one pyramid set to every batch entry
+  long long ws_face_stride;   // floats per face in ws
+  int log2n, faces, band, out_face_stride, num_faces;
+  FaceParam fp[kMaxFacesPerLaunch];
+};
+
+// Tiling constants of the 2D tile kernel.
+constexpr int kTileKF = 3;    // fine levels per tile: the tile root level is c = max(0, m - KF)
+constexpr int kTileTC = 8;    // tile side at level c (cells)
+
+inline int coarse_level(int m) { return m > kTileKF ? m - kTileKF : 0; }
+inline long long ws_face_floats_2d(int n) {
+  int c = coarse_level(n);
+  long long a = 3ll << (2 * c);
+  long long b = c > 0 ? (3ll << (2 * (c - 1))) : 0;
+  return a + b;
+}
+
+size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces);
+hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int faces,
+                       long long num_faces, long long in_batch_stride, const double* shifts_host,
+                       const float* shifts_dev_per_vertex, FaceParam* dev_fp_buf, int band,
+                       void* ws, size_t ws_bytes, cudaStream_t st);
+
+// ----------------------------------------------------------------------------------- relight
+
+hs_status launch_relight(const float* T, long long V, int faces, int kface, const float* L,
+                         long long lstride, int batch, float* R, cudaStream_t st);
+hs_status launch_rowdot(const float* T, const float* S, long long rows, long long K, float* R,
+                        cudaStream_t st);
+hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
+                               int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
+
+}  // namespace hs

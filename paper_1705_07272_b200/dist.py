@@ -1,0 +1,111 @@
+"""Multi-GPU data parallelism over vertex rows.
+
+One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
+
+* vertex rows are contiguous blocks [start_r, start_r + count_r) per rank (``shard_rows``); the
+  transfer rows T are generated in place on their rank from the counter hash keyed by the GLOBAL
+  row id, so every shard is bitwise the 1-GPU matrix's slice and never moves;
+* the shifted lighting band is computed once (rank 0, ``haar_shift_coeffs``) and broadcast
+  (``dist.broadcast`` over NVLink) -- the one exchange step into the relight;
+* radiance is gathered to rank 0 chunk by chunk: chunk i is gathered on the NCCL stream while
+  chunk i+1 is relit (``relight_and_gather``), so the gather overlaps the HBM-bound relight.
+
+Per-row results do not depend on the sharding (each row's reduction order is fixed inside the
+kernels), so the gathered R equals the 1-GPU R bit for bit.
+
+The compute step is injected (``relight_fn``) so the communication logic is testable on CPU with
+gloo; on the GPU it is always the C-ABI ``relight_vertices``.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous near-equal blocks: the first (total % world) ranks get one extra row."""
+    if world < 1 or not (0 <= rank < world) or total < 0:
+        raise ValueError("bad shard arguments")
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    count = base + (1 if rank < extra else 0)
+    return start, count
+
+
+def max_shard(total: int, world: int) -> int:
+    return -(-total // world)
+
+
+def chunk_bounds(count: int, chunks: int) -> List[Tuple[int, int]]:
+    """Split [0, count) into ``chunks`` contiguous near-equal pieces (empty pieces dropped)."""
+    chunks = max(1, min(chunks, max(count, 1)))
+    out = []
+    for c in range(chunks):
+        s, n = shard_rows(count, chunks, c)
+        if n > 0:
+            out.append((s, n))
+    return out
+
+
+def broadcast_band(band: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """Broadcast the shifted lighting band (rank ``src`` computed it) to every rank in place."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(band, src=src, group=group)
+    return band
+
+
+def relight_and_gather(transfer_local: torch.Tensor, band: torch.Tensor, total_rows: int,
+                       relight_fn: Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None],
+                       radiance_full: Optional[torch.Tensor] = None, chunks: int = 4,
+                       gather: bool = True, group=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
+    """Relight this rank's rows chunk by chunk and gather radiance into rank 0, overlapping the
+    gather of chunk i with the relight of chunk i+1.
+
+    transfer_local: [count_r][K] this rank's rows; band: [B][F][stride] (already broadcast);
+    relight_fn(T_chunk, band, R_chunk_out) fills R_chunk_out [rows][B].
+    radiance_full (rank 0, [total_rows][B]) receives every rank's rows at their global offsets.
+    Returns (local radiance [count_r][B], radiance_full or None).
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    B = band.shape[0]
+    start, count = shard_rows(total_rows, world, rank)
+    if transfer_local.shape[0] != count:
+        raise ValueError(f"rank {rank}: expected {count} transfer rows, got {transfer_local.shape[0]}")
+    local = torch.empty((count, B), dtype=torch.float32, device=transfer_local.device)
+    if world == 1 or not gather:
+        for s, n in chunk_bounds(count, chunks):
+            relight_fn(transfer_local[s:s + n], band, local[s:s + n])
+        if world == 1 and radiance_full is not None:
+            radiance_full.copy_(local)
+        return local, radiance_full
+    # every rank runs the same chunk schedule: chunk c of every rank has the same size when shards
+    # are padded to max_shard -> one all_gather per chunk (NCCL collectives need equal sizes)
+    ms = max_shard(total_rows, world)
+    sched = chunk_bounds(ms, chunks)
+    recv = None
+    if rank == 0:
+        if radiance_full is None:
+            radiance_full = torch.empty((total_rows, B), dtype=torch.float32, device=transfer_local.device)
+    pending = []
+    for s, n in sched:
+        lo, hi = min(s, count), min(s + n, count)
+        if hi > lo:
+            relight_fn(transfer_local[lo:hi], band, local[lo:hi])
+        send = torch.zeros((n, B), dtype=torch.float32, device=local.device)
+        if hi > lo:
+            send[: hi - lo].copy_(local[lo:hi])
+        recv = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+        work = dist.gather(send, gather_list=recv, dst=0, group=group, async_op=True)
+        pending.append((work, s, n, recv, send))
+    for work, s, n, recv_l, _send in pending:
+        work.wait()
+        if rank == 0:
+            for r in range(world):
+                rs, rc = shard_rows(total_rows, world, r)
+                lo, hi = min(s, rc), min(s + n, rc)
+                if hi > lo:
+                    radiance_full[rs + lo:rs + hi].copy_(recv_l[r][: hi - lo])
+    return local, radiance_full

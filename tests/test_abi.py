@@ -1,0 +1,122 @@
+"""C-ABI library checks that need no GPU (-m "not gpu"): the library loads, exports every symbol
+include/haarshift.h declares, and validates arguments before touching the device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "haarshift.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1705_07272_b200 import _lib
+    return _lib.load()
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return re.findall(r"HS_API\s+[\w\s\*]+?\b(\w+)\s*\(", txt)
+
+
+def test_header_declares_expected_entry_points():
+    syms = set(declared_symbols())
+    for s in ["haar_shift_coeffs", "relight_vertices", "relight_vertices_shifted", "haar_shift_workspace_bytes",
+              "relight_shifted_workspace_bytes", "hs_fill_transfer", "hs_status_string", "hs_last_cuda_error",
+              "hs_abi_version", "hs_last_launch_count"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    from paper_1705_07272_b200 import _lib
+    assert set(declared_symbols()) == set(_lib.SIGNATURES)
+
+
+def test_status_strings_and_version(lib):
+    assert lib.hs_abi_version() == 1
+    assert [lib.hs_status_string(i).decode() for i in range(5)] == [
+        "HS_OK", "HS_ERR_INVALID_ARG", "HS_ERR_ALIGNMENT", "HS_ERR_UNSUPPORTED", "HS_ERR_CUDA"]
+
+
+def test_workspace_sizes(lib):
+    assert lib.haar_shift_workspace_bytes(1, 3, 1, 1) == 0
+    w = lib.haar_shift_workspace_bytes(2, 8, 6, 64)
+    # counters (aligned 256) + per face 3*4^5 + 3*4^4 floats
+    assert w == ((384 * 4 + 255) // 256) * 256 + 384 * (3 * 1024 + 3 * 256) * 4
+    assert lib.haar_shift_workspace_bytes(2, 0, 1, 1) == 0
+    assert lib.haar_shift_workspace_bytes(2, 13, 1, 1) == 0
+    assert lib.relight_shifted_workspace_bytes(100000, 6, 7) > 128 * 6 * 16384 * 4
+
+
+FAKE = 1 << 20  # an aligned, never-dereferenced "device" address
+
+
+def _shifts(n):
+    a = np.zeros(n, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+def test_shift_validation_before_device(lib):
+    a, p = _shifts(64)
+    f = lib.haar_shift_coeffs
+    assert f(None, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1        # null in
+    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, None, 3, FAKE * 8, 1 << 20, None) == 1      # null shifts
+    assert f(FAKE, FAKE * 4, 3, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1         # ndim
+    assert f(FAKE, FAKE * 4, 2, 0, 1, 1, p, 0, FAKE * 8, 1 << 20, None) == 1         # log2n
+    assert f(FAKE, FAKE * 4, 2, 13, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1        # log2n
+    assert f(FAKE, FAKE * 4, 2, 3, 0, 1, p, 3, FAKE * 8, 1 << 20, None) == 1         # faces
+    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 4, FAKE * 8, 1 << 20, None) == 1         # band > log2n
+    assert f(FAKE, FAKE, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1             # in == out
+    assert f(FAKE, FAKE + 64, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1        # overlap
+    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, None, 0, None) == 1                   # no workspace
+    a[1] = np.nan
+    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1         # non-finite shift
+    a[1] = np.inf
+    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1
+    a[1] = 0.0
+    assert f(FAKE + 4, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 2     # misaligned
+
+
+def test_relight_validation_before_device(lib):
+    f = lib.relight_vertices
+    assert f(None, 10, 6, 16, FAKE, 16, 1, FAKE * 2, None) == 1
+    assert f(FAKE, 0, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # V
+    assert f(FAKE, 10, 6, 8, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # k_face not 4^k
+    assert f(FAKE, 10, 6, 1, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # k_face < 4
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 8, 1, FAKE * 4, None) == 1                 # stride < k_face
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 18, 1, FAKE * 4, None) == 1                # stride % 4
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 0, FAKE * 4, None) == 1                # batch
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1025, FAKE * 4, None) == 1
+    assert f(FAKE + 8, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None) == 2            # misaligned
+    g = lib.relight_vertices_shifted
+    assert g(FAKE, 10, 6, FAKE * 2, 3, None, FAKE * 4, FAKE * 8, 1 << 30, None) == 1
+    assert g(FAKE, 10, 6, FAKE * 2, 3, FAKE * 3, FAKE * 4, FAKE * 8, 16, None) == 1  # small workspace
+    h = lib.hs_fill_transfer
+    assert h(None, 0, 1, 6, 16, 1, 2, None) == 1
+    assert h(FAKE, 0, 1, 6, 12, 1, 2, None) == 1
+
+
+def test_no_device_fails_loudly(lib):
+    """Valid arguments on a host without a usable sm_100 device: an error status, never a silent
+    CPU computation."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except Exception:
+        pass
+    a, p = _shifts(64)
+    st = lib.haar_shift_coeffs(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None)
+    assert st in (3, 4)
+    st = lib.relight_vertices(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None)
+    assert st in (3, 4)
+    from paper_1705_07272_b200 import _lib
+    with pytest.raises(_lib.HaarShiftError):
+        _lib.check("relight_vertices", st)
