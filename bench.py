@@ -225,6 +225,10 @@ def run_ours(args, cfg):
     ws = torch.empty(hs.haar_shift_workspace_bytes(2, n, F, B), dtype=torch.uint8, device=dev)
     R = torch.empty((rows, B), dtype=torch.float32, device=dev)
     R_full = torch.empty((V, B), dtype=torch.float32, device=dev) if (rank == 0 and world > 1) else None
+    rws_bytes = hs.relight_workspace_bytes(F, kf, B)
+    rws = torch.empty(rws_bytes + 1024, dtype=torch.uint8, device=dev) if rws_bytes else None
+    if rws is not None:
+        rws = rws[(-rws.data_ptr()) % 1024:]
     stream = torch.cuda.current_stream()
     launches = {"n": 0}
     rel_events = []
@@ -233,7 +237,7 @@ def run_ours(args, cfg):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        hs.relight_vertices(Tc, band, F, kf, out=Rc)
+        hs.relight_vertices(Tc, band, F, kf, out=Rc, workspace=rws)
         e1.record(stream)
         launches["n"] += hs.last_launch_count()
         rel_events.append((e0, e1, Tc.shape[0]))

@@ -106,12 +106,19 @@ HS_API size_t haar_shift_workspace_bytes(int ndim, int log2n, int faces, int bat
  *   k_face        a power of 4 (the HAAR1 prefix 4^k: scaling + levels < k), >= 4.
  *   batch         1 .. 1024 light/rotation frames.
  *   radiance      [num_vertices][batch] fp32.
- * Accumulation is fp32 (batch <= 8: CUDA-core streaming GEMV; batch multiple of 64: tcgen05
- * split-precision GEMM with fp32-level accuracy; other batches: CUDA-core tiled GEMM).
+ *   workspace     device scratch of >= relight_workspace_bytes(faces, k_face, batch) bytes,
+ *                 1024-byte aligned (may be NULL when that size is 0).
+ * Accumulation is fp32.  batch <= 8: CUDA-core streaming GEMV.  batch a multiple of 64 with
+ * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16 (T and the
+ * per-frame-scaled light each split into fp16 hi + lo, three products, fp32 accumulation in TMEM;
+ * ~2^-21 relative per product; requires |T| < 2^15 -- transfer coefficients of an orthonormal
+ * basis are bounded by the function's L2 norm).  Other batches: CUDA-core tiled GEMM.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
                            const float* light, int64_t light_face_stride, int batch,
-                           float* radiance, void* stream);
+                           float* radiance, void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t relight_workspace_bytes(int faces, int k_face, int batch);
 
 /* ---------------------------------------------------------------------------------------------
  * relight_vertices_shifted -- fused per-vertex shift + relight:

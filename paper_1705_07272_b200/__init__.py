@@ -21,12 +21,13 @@ from .api import (  # noqa: F401
     last_launch_count,
     relight_shifted_workspace_bytes,
     relight_vertices,
+    relight_workspace_bytes,
     relight_vertices_shifted,
     shift_and_relight,
 )
 
 __all__ = [
     "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_workspace_bytes", "hs_fill_transfer",
-    "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_vertices_shifted",
+    "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
     "shift_and_relight",
 ]

@@ -77,8 +77,13 @@ def haar_shift_coeffs(coeffs: torch.Tensor, shifts, ndim: int = 2, band_levels: 
     return out
 
 
+def relight_workspace_bytes(faces: int, k_face: int, batch: int) -> int:
+    return int(load().relight_workspace_bytes(faces, k_face, batch))
+
+
 def relight_vertices(transfer: torch.Tensor, light: torch.Tensor, faces: int, k_face: int,
-                     out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+                     out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """transfer [V][faces*k_face], light [batch][faces][stride >= k_face] -> radiance [V][batch]."""
     lib = load()
     _dev_f32(transfer, "transfer")
@@ -92,8 +97,17 @@ def relight_vertices(transfer: torch.Tensor, light: torch.Tensor, faces: int, k_
     if out is None:
         out = torch.empty((V, B), dtype=torch.float32, device=transfer.device)
     _dev_f32(out, "out")
+    need = relight_workspace_bytes(faces, k_face, B)
+    ws_ptr = None
+    if need:
+        if workspace is None or workspace.numel() * workspace.element_size() < need or workspace.data_ptr() % 1024:
+            workspace = torch.empty(need, dtype=torch.uint8, device=transfer.device)   # allocator: 512B+ aligned
+            if workspace.data_ptr() % 1024:
+                workspace = torch.empty(need + 1024, dtype=torch.uint8, device=transfer.device)
+                workspace = workspace[(-workspace.data_ptr()) % 1024:]
+        ws_ptr = workspace.data_ptr()
     st = lib.relight_vertices(transfer.data_ptr(), V, faces, k_face, light.data_ptr(), stride, B, out.data_ptr(),
-                              _stream_ptr(stream))
+                              ws_ptr, need, _stream_ptr(stream))
     check("relight_vertices", st)
     return out
 
@@ -136,10 +150,11 @@ def hs_fill_transfer(out: torch.Tensor, row_start: int, faces: int, k_face: int,
 
 def shift_and_relight(light: torch.Tensor, shifts, transfer: torch.Tensor, faces: int, k_face: int,
                       band_levels: int, shifted: Optional[torch.Tensor] = None, radiance: Optional[torch.Tensor] = None,
-                      workspace: Optional[torch.Tensor] = None,
+                      workspace: Optional[torch.Tensor] = None, relight_workspace: Optional[torch.Tensor] = None,
                       stream: Optional[torch.cuda.Stream] = None):
     """One step of the hot path: shift every frame's pyramids in the Haar domain (band only), then
     relight every vertex with the shifted band.  Returns (shifted band, radiance)."""
     shifted = haar_shift_coeffs(light, shifts, 2, band_levels, out=shifted, workspace=workspace, stream=stream)
-    radiance = relight_vertices(transfer, shifted, faces, k_face, out=radiance, stream=stream)
+    radiance = relight_vertices(transfer, shifted, faces, k_face, out=radiance, workspace=relight_workspace,
+                                stream=stream)
     return shifted, radiance

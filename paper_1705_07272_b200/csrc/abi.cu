@@ -116,9 +116,14 @@ hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, in
   return s;
 }
 
+size_t relight_workspace_bytes(int faces, int k_face, int batch) {
+  if (faces < 1 || batch < 1 || batch > 1024 || !is_pow4(k_face) || k_face < 4) return 0;
+  return relight_tc_workspace_bytes(faces, k_face, batch);
+}
+
 hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
                            const float* light, int64_t light_face_stride, int batch, float* radiance,
-                           void* stream) {
+                           void* workspace, size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
   g_launches = 0;
   if (!transfer || !light || !radiance) return HS_ERR_INVALID_ARG;
@@ -126,11 +131,15 @@ hs_status relight_vertices(const float* transfer, int64_t num_vertices, int face
   if (!is_pow4(k_face) || k_face < 4 || k_face > (1 << (2 * HS_MAX_LOG2N))) return HS_ERR_INVALID_ARG;
   if (light_face_stride < k_face || (light_face_stride & 3)) return HS_ERR_INVALID_ARG;
   if ((long long)faces * k_face > (1ll << 30)) return HS_ERR_INVALID_ARG;
-  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance)) return HS_ERR_ALIGNMENT;
+  const size_t need = relight_tc_workspace_bytes(faces, k_face, batch);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance) ||
+      (need > 0 && (reinterpret_cast<uintptr_t>(workspace) & 1023)))
+    return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
   if (s != HS_OK) return s;
-  s = launch_relight(transfer, num_vertices, faces, k_face, light, light_face_stride, batch, radiance,
-                     (cudaStream_t)stream);
+  s = launch_relight(transfer, num_vertices, faces, k_face, light, light_face_stride, batch, radiance, workspace,
+                     workspace_bytes, (cudaStream_t)stream);
   g_last_launches = g_launches;
   return s;
 }

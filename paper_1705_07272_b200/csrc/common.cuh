@@ -141,7 +141,8 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
 // ----------------------------------------------------------------------------------- relight
 
 hs_status launch_relight(const float* T, long long V, int faces, int kface, const float* L,
-                         long long lstride, int batch, float* R, cudaStream_t st);
+                         long long lstride, int batch, float* R, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t relight_tc_workspace_bytes(int faces, int kface, int batch);
 hs_status launch_rowdot(const float* T, const float* S, long long rows, long long K, float* R,
                         cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,

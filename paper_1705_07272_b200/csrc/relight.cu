@@ -6,8 +6,8 @@
 //    128-bit non-allocating loads; each warp owns RPW rows so a light float4 (L1/L2 resident) is
 //    reused across RPW rows; per-row reduction order is fixed (independent of the row count and of
 //    multi-GPU sharding).
-//  * other batches: CUDA-core tiled GEMM (128 rows x 64 frames x 32 k) -- the fallback; batches
-//    that are multiples of 64 go to the tcgen05 kernel (relight_tc.cu).
+//  * batches that are multiples of 64 (and K % 64 == 0): the tcgen05 split-precision kernel
+//    (relight_tc.cu); other batches: CUDA-core tiled GEMM (128 rows x 64 frames x 32 k).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -204,11 +204,11 @@ hs_status gemv(const float* T, long long V, int K, int kshift, const float* L, l
 
 }  // namespace
 
-hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, const float* L,
-                            long long lstride, int batch, float* R, cudaStream_t st, bool* handled);
+hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, const float* L, long long lstride,
+                            int batch, float* R, void* ws, size_t ws_bytes, cudaStream_t st, bool* handled);
 
 hs_status launch_relight(const float* T, long long V, int faces, int kface, const float* L,
-                         long long lstride, int batch, float* R, cudaStream_t st) {
+                         long long lstride, int batch, float* R, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int K = faces * kface;
   int kshift = 0;
   while ((1 << kshift) < kface) ++kshift;
@@ -225,7 +225,7 @@ hs_status launch_relight(const float* T, long long V, int faces, int kface, cons
     default: break;
   }
   bool handled = false;
-  hs_status s = launch_relight_tc(T, V, faces, kface, L, lstride, batch, R, st, &handled);
+  hs_status s = launch_relight_tc(T, V, faces, kface, L, lstride, batch, R, ws, ws_bytes, st, &handled);
   if (handled || s != HS_OK) return s;
   dim3 grid((unsigned)((V + GM - 1) / GM), (unsigned)((batch + GN - 1) / GN));
   relight_gemm_kernel<<<grid, 256, 0, st>>>(T, V, K, kshift, L, lstride, lbatch, batch, R);

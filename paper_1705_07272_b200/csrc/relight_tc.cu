@@ -1,11 +1,463 @@
-// tcgen05 split-precision relight GEMM for batch % 64 == 0 -- placeholder until
-// the tensor-core kernel lands; reports "not handled" so the CUDA-core tiled GEMM runs.
+// Relight on the 5th-generation tensor cores (batch % 64 == 0):
+//   R[v][b] = sum_k T[v][k] L[b][k]        (double product, PAPER.md eq:tripleSum P:253-266)
+// in split-precision fp16 with fp32 accumulation in TMEM, accurate to ~2^-21 relative per
+// product:
+//   T = T_hi + 2^-11 T_lo,  L_b s_b = L_hi + 2^-11 L_lo   (fp16 pieces, s_b a per-frame power of 2)
+//   acc_hh = sum T_hi L_hi,  acc_x = sum (T_hi L_lo + T_lo L_hi),
+//   R = (acc_hh + 2^-11 acc_x) / s_b          (the dropped T_lo L_lo term is ~2^-22)
+//
+// Kernel anatomy (one CTA per SM, persistent over 128-row tiles, 12 warps):
+//   warp 0      TMA producer: T tile [128 rows x 64 k] fp32 (two 128B-swizzled boxes) + the
+//               pre-swizzled [L_hi | L_lo] band tile [128 x 64] fp16 (one bulk copy) per stage;
+//   warp 1      MMA issuer (one thread): per 16-k step, tcgen05.mma kind::f16 with A from TMEM:
+//                 D[acc_hh | acc_x] (N=128) += T_hi x [L_hi | L_lo];  D[acc_x] (N=64) += T_lo x L_hi
+//   warp 2      TMEM allocator (512 columns: 4 A stages x 64 + 2 accumulator buffers x 128);
+//   warps 4-7   converters: read their row of the T tile from smem, split fp32 -> fp16 hi/lo and
+//               tcgen05.st them into the A stage (lane = row) -- T never round-trips through HBM;
+//   warps 8-11  epilogue: tcgen05.ld both accumulators, combine, scale, store R rows; the two
+//               accumulator buffers let the epilogue of tile i overlap the MMAs of tile i+1.
+// All hand-offs are mbarriers; tcgen05.commit signals MMA completion.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 
 namespace hs {
-hs_status launch_relight_tc(const float*, long long, int, int, const float*, long long, int, float*,
-                            cudaStream_t, bool* handled) {
+namespace {
+
+constexpr int BM = 128;           // rows per tile (MMA M)
+constexpr int BK = 64;            // k per stage
+constexpr int BN = 64;            // frames per block (MMA N of each accumulator)
+constexpr int STAGES = 4;         // smem stages
+constexpr int ASTAGES = 4;        // TMEM A stages
+constexpr int T_STAGE = BM * BK * 4;         // 32 KB
+constexpr int L_STAGE = 2 * BN * BK * 2;     // 16 KB: [L_hi 64 rows | L_lo 64 rows] x 128 B
+constexpr int SMEM_TILES = STAGES * (T_STAGE + L_STAGE);
+constexpr int SMEM_BYTES = SMEM_TILES + 1024 /*align*/ + 256 /*barriers*/ + BN * 4 + 64;
+constexpr int kThreads = 384;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t ACC_COL0 = ASTAGES * 64;  // 256
+
+// ------------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle (8-row groups 1024 B apart).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major) = 1
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO = 1024 B
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D f32, A/B f16, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------- prologue
+// One CTA per frame: per-frame power-of-2 scale s_b (max |L_b s_b| in [2^14, 2^15)), then the
+// fp16 hi/lo split of L_b s_b written into pre-swizzled 16 KB tiles [L_hi 64 rows | L_lo 64 rows]
+// per (frame block, k block) -- exactly the 128B-swizzled K-major smem image the MMA reads.
+__global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __restrict__ L, long long lstride,
+                                                               int faces, int kshift, int K, uint8_t* __restrict__ tiles,
+                                                               float* __restrict__ inv_scale) {
+  const int b = blockIdx.x;
+  const int fb = b / BN, r = b % BN;
+  const int kmask = (1 << kshift) - 1;
+  const float* Lb = L + (long long)b * faces * lstride;
+  __shared__ float red[8];
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(Lb + (long long)(k >> kshift) * lstride + (k & kmask))));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
+  int e = 0;
+  if (mx > 0.f && isfinite(mx)) e = 14 - ilogbf(mx);
+  e = max(-120, min(120, e));
+  const float s = ldexpf(1.f, e);
+  if (threadIdx.x == 0) inv_scale[b] = ldexpf(1.f, -e);
+  const int nkb = K / BK;
+  for (int c8 = threadIdx.x; c8 < K / 8; c8 += blockDim.x) {
+    const int k0 = c8 * 8;
+    const int kb = k0 / BK, c = (k0 % BK) / 8;
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int k = k0 + 2 * p;
+      const float v0 = __ldg(Lb + (long long)(k >> kshift) * lstride + (k & kmask)) * s;
+      const float v1 = __ldg(Lb + (long long)((k + 1) >> kshift) * lstride + ((k + 1) & kmask)) * s;
+      const __half2 h = __floats2half2_rn(v0, v1);
+      const float2 hf = __half22float2(h);
+      const __half2 l = __floats2half2_rn((v0 - hf.x) * 2048.f, (v1 - hf.y) * 2048.f);
+      hi[p] = *reinterpret_cast<const uint32_t*>(&h);
+      lo[p] = *reinterpret_cast<const uint32_t*>(&l);
+    }
+    uint8_t* tile = tiles + ((long long)fb * nkb + kb) * L_STAGE;
+    const int off = r * 128 + ((c ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(tile + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(tile + BN * 128 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// ------------------------------------------------------------------------------- main kernel
+__global__ void __launch_bounds__(kThreads, 1)
+    relight_tc_kernel(const __grid_constant__ CUtensorMap tmapT, const uint8_t* __restrict__ ltiles,
+                      const float* __restrict__ inv_scale_g, float* __restrict__ R, long long V, int K, int B,
+                      int ntiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sT = smem;                                  // STAGES x 32 KB
+  uint8_t* sL = smem + STAGES * T_STAGE;               // STAGES x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_TILES);
+  uint64_t* full = bars;                               // [STAGES]   TMA -> converters + MMA
+  uint64_t* empty = bars + STAGES;                     // [STAGES]   converters (128) + MMA commit (1)
+  uint64_t* afull = bars + 2 * STAGES;                 // [ASTAGES]  converters -> MMA
+  uint64_t* aempty = bars + 2 * STAGES + ASTAGES;      // [ASTAGES]  MMA commit -> converters
+  uint64_t* tfull = bars + 2 * STAGES + 2 * ASTAGES;   // [2]        MMA commit -> epilogue
+  uint64_t* tempty = tfull + 2;                        // [2]        epilogue (128) -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = K / BK;
+  const int nfb = B / BN;
+  const long long nwork = (long long)ntiles * nfb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 129);
+    }
+    for (int s = 0; s < ASTAGES; ++s) {
+      mbar_init(&afull[s], 128);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmapT) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int tile = (int)(w / nfb), fb = (int)(w % nfb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], T_STAGE + L_STAGE);
+          uint8_t* dT = sT + stage * T_STAGE;
+          tma_load_2d(dT, &tmapT, kb * BK, tile * BM, &full[stage]);
+          tma_load_2d(dT + T_STAGE / 2, &tmapT, kb * BK + 32, tile * BM, &full[stage]);
+          bulk_load(sL + stage * L_STAGE, ltiles + ((long long)fb * nkb + kb) * L_STAGE, L_STAGE, &full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, astage = 0;
+      uint32_t phase = 0, aphase = 0;
+      int it = 0;
+      const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
+      for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t accph = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], accph ^ 1);
+        fence_after();
+        const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&afull[astage], aphase);
+          fence_after();
+          const uint32_t lbase = smem_u32(sL + stage * L_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t bd = sw128_desc(lbase + kk * 32);
+            const uint32_t ahi = tmem + astage * 64 + kk * 8;
+            tc_mma_ts(dhh, ahi, bd, id128, (kb | kk) != 0);      // [acc_hh | acc_x] += T_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);          // acc_x += T_lo x L_hi
+          }
+          tc_commit(&empty[stage]);
+          tc_commit(&aempty[astage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++astage == ASTAGES) {
+            astage = 0;
+            aphase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------------ converters
+    const int row = threadIdx.x - 128;     // 0..127 = TMEM lane
+    const int q = warp & 3;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    int stage = 0, astage = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&aempty[astage], aphase ^ 1);
+        fence_after();
+        const uint8_t* tb = sT + stage * T_STAGE;
+#pragma unroll
+        for (int box = 0; box < 2; ++box) {
+          uint32_t hi[16], lo[16];
+          const uint8_t* rowp = tb + box * (T_STAGE / 2) + row * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
+            const __half2 h0 = __floats2half2_rn(v.x, v.y);
+            const __half2 h1 = __floats2half2_rn(v.z, v.w);
+            const float2 f0 = __half22float2(h0);
+            const float2 f1 = __half22float2(h1);
+            const __half2 l0 = __floats2half2_rn((v.x - f0.x) * 2048.f, (v.y - f0.y) * 2048.f);
+            const __half2 l1 = __floats2half2_rn((v.z - f1.x) * 2048.f, (v.w - f1.y) * 2048.f);
+            hi[2 * c] = *reinterpret_cast<const uint32_t*>(&h0);
+            hi[2 * c + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+            lo[2 * c] = *reinterpret_cast<const uint32_t*>(&l0);
+            lo[2 * c + 1] = *reinterpret_cast<const uint32_t*>(&l1);
+          }
+          tmem_st16(lane_base + astage * 64 + box * 16, hi);
+          tmem_st16(lane_base + astage * 64 + 32 + box * 16, lo);
+        }
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&afull[astage]);
+        mbar_arrive(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++astage == ASTAGES) {
+          astage = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------------ epilogue
+    const int row = threadIdx.x - 256;
+    const int q = warp & 3;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    int it = 0;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
+      const int tile = (int)(w / nfb), fb = (int)(w % nfb);
+      const int acc = it & 1;
+      const uint32_t accph = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], accph);
+      fence_after();
+      const long long grow = (long long)tile * BM + row;
+      float* out = R + grow * B + fb * BN;
+#pragma unroll
+      for (int c = 0; c < BN / 16; ++c) {
+        float hh[16], xx[16];
+        tmem_ld16(lane_base + ACC_COL0 + acc * 128 + c * 16, hh);
+        tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
+        tmem_wait_ld();
+        if (grow < V) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            float4 o;
+            o.x = fmaf(xx[j + 0], 1.f / 2048.f, hh[j + 0]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 0);
+            o.y = fmaf(xx[j + 1], 1.f / 2048.f, hh[j + 1]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 1);
+            o.z = fmaf(xx[j + 2], 1.f / 2048.f, hh[j + 2]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 2);
+            o.w = fmaf(xx[j + 3], 1.f / 2048.f, hh[j + 3]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 3);
+            *reinterpret_cast<float4*>(out + c * 16 + j) = o;
+          }
+        }
+      }
+      fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+bool relight_tc_eligible(int faces, int kface, int batch) {
+  const long long K = (long long)faces * kface;
+  return batch % BN == 0 && K % BK == 0 && K >= BK;
+}
+
+size_t relight_tc_workspace_bytes(int faces, int kface, int batch) {
+  if (!relight_tc_eligible(faces, kface, batch)) return 0;
+  const long long K = (long long)faces * kface;
+  return (size_t)(batch / BN) * (size_t)(K / BK) * L_STAGE + (size_t)batch * sizeof(float) + 256;
+}
+
+hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, const float* L, long long lstride,
+                            int batch, float* R, void* ws, size_t ws_bytes, cudaStream_t st, bool* handled) {
   *handled = false;
+  if (!relight_tc_eligible(faces, kface, batch)) return HS_OK;
+  const size_t need = relight_tc_workspace_bytes(faces, kface, batch);
+  if (!ws || ws_bytes < need) return HS_OK;  // caller passed no workspace: CUDA-core path
+  PFN_cuTensorMapEncodeTiled_v12000 encode = get_encode();
+  if (!encode) return HS_OK;
+  const int K = faces * kface;
+  int kshift = 0;
+  while ((1 << kshift) < kface) ++kshift;
+  uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
+  float* inv = reinterpret_cast<float*>(tiles + (size_t)(batch / BN) * (size_t)(K / BK) * L_STAGE);
+
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {(cuuint64_t)K, (cuuint64_t)V};
+  const cuuint64_t gstride[1] = {(cuuint64_t)K * 4};
+  const cuuint32_t box[2] = {32, BM};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(T), gdim, gstride, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(T)");
+    return HS_ERR_CUDA;
+  }
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(relight_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
+  HS_CHECK_CUDA(attr_err, "cudaFuncSetAttribute(relight_tc_kernel)");
+
+  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv);
+  HS_CHECK_LAUNCH("relight_tc_prep_kernel");
+  const int ntiles = (int)((V + BM - 1) / BM);
+  const long long nwork = (long long)ntiles * (batch / BN);
+  const int grid = (int)(nwork < num_sms() ? nwork : num_sms());
+  relight_tc_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(map, tiles, inv, R, V, K, batch, ntiles);
+  HS_CHECK_LAUNCH("relight_tc_kernel");
+  *handled = true;
   return HS_OK;
 }
+
 }  // namespace hs

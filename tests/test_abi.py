@@ -27,7 +27,7 @@ def declared_symbols():
 def test_header_declares_expected_entry_points():
     syms = set(declared_symbols())
     for s in ["haar_shift_coeffs", "relight_vertices", "relight_vertices_shifted", "haar_shift_workspace_bytes",
-              "relight_shifted_workspace_bytes", "hs_fill_transfer", "hs_status_string", "hs_last_cuda_error",
+              "relight_shifted_workspace_bytes", "relight_workspace_bytes", "hs_fill_transfer", "hs_status_string", "hs_last_cuda_error",
               "hs_abi_version", "hs_last_launch_count"]:
         assert s in syms
 
@@ -86,15 +86,21 @@ def test_shift_validation_before_device(lib):
 
 def test_relight_validation_before_device(lib):
     f = lib.relight_vertices
-    assert f(None, 10, 6, 16, FAKE, 16, 1, FAKE * 2, None) == 1
-    assert f(FAKE, 0, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # V
-    assert f(FAKE, 10, 6, 8, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # k_face not 4^k
-    assert f(FAKE, 10, 6, 1, FAKE * 2, 16, 1, FAKE * 4, None) == 1                 # k_face < 4
-    assert f(FAKE, 10, 6, 16, FAKE * 2, 8, 1, FAKE * 4, None) == 1                 # stride < k_face
-    assert f(FAKE, 10, 6, 16, FAKE * 2, 18, 1, FAKE * 4, None) == 1                # stride % 4
-    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 0, FAKE * 4, None) == 1                # batch
-    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1025, FAKE * 4, None) == 1
-    assert f(FAKE + 8, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None) == 2            # misaligned
+    W = FAKE * 16
+    assert f(None, 10, 6, 16, FAKE, 16, 1, FAKE * 2, None, 0, None) == 1
+    assert f(FAKE, 0, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None, 0, None) == 1       # V
+    assert f(FAKE, 10, 6, 8, FAKE * 2, 16, 1, FAKE * 4, None, 0, None) == 1       # k_face not 4^k
+    assert f(FAKE, 10, 6, 1, FAKE * 2, 16, 1, FAKE * 4, None, 0, None) == 1       # k_face < 4
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 8, 1, FAKE * 4, None, 0, None) == 1       # stride < k_face
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 18, 1, FAKE * 4, None, 0, None) == 1      # stride % 4
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 0, FAKE * 4, None, 0, None) == 1      # batch
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1025, FAKE * 4, None, 0, None) == 1
+    assert f(FAKE + 8, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None, 0, None) == 2  # misaligned
+    need = lib.relight_workspace_bytes(6, 1024, 64)
+    assert need >= 64 * 6144 * 4                                                   # fp16 hi+lo light tiles
+    assert lib.relight_workspace_bytes(6, 16, 1) == 0
+    assert f(FAKE, 10, 6, 1024, FAKE * 2, 1024, 64, FAKE * 4, None, 0, None) == 1  # tensor path needs ws
+    assert f(FAKE, 10, 6, 1024, FAKE * 2, 1024, 64, FAKE * 4, W + 512, need, None) == 2  # ws 1024-aligned
     g = lib.relight_vertices_shifted
     assert g(FAKE, 10, 6, FAKE * 2, 3, None, FAKE * 4, FAKE * 8, 1 << 30, None) == 1
     assert g(FAKE, 10, 6, FAKE * 2, 3, FAKE * 3, FAKE * 4, FAKE * 8, 16, None) == 1  # small workspace
@@ -115,7 +121,7 @@ def test_no_device_fails_loudly(lib):
     a, p = _shifts(64)
     st = lib.haar_shift_coeffs(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None)
     assert st in (3, 4)
-    st = lib.relight_vertices(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None)
+    st = lib.relight_vertices(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4, None, 0, None)
     assert st in (3, 4)
     from paper_1705_07272_b200 import _lib
     with pytest.raises(_lib.HaarShiftError):
