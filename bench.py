@@ -22,7 +22,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -46,7 +45,7 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c5")
@@ -67,57 +66,64 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 100 ms during the timed region."""
+    """SM clock and clock-event (throttle) reasons polled through NVML every ~2 ms on a background
+    thread; ``mark(True/False)`` brackets the timed region and ``summary()`` reports the samples
+    taken inside it (the nvidia-smi CLI cannot sample a region this short)."""
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.samples = []          # (t, sm_mhz, reasons_mask, in_region)
+        self.in_region = False
+        self.stop = False
         self.thread = None
+        self.max_mhz = None
+        self.err = None
 
     def __enter__(self):
-        cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active", "--format=csv,noheader,nounits",
-               "-lms", "100"]
         try:
-            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 3:
-                self.rows.append(parts)
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self.stop:
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                mask = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((time.perf_counter(), mhz, mask, self.in_region))
+            except Exception as e:  # pragma: no cover
+                self.err = repr(e)
+                return
+            time.sleep(0.002)
+
+    def mark(self, inside: bool):
+        self.in_region = inside
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop = True
         if self.thread is not None:
             self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        for r in self.rows:
-            try:
-                sm.append(float(r[0]))
-                mx = float(r[1])
-                mask = int(r[2], 16) if r[2].startswith("0x") else int(r[2])
-                for bit, name in REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        reasons.add(name)
-            except ValueError:
-                continue
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [s for s in self.samples if s[3]]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
+                    "error": self.err}
+        reasons = set()
+        for _, _, mask, _ in inside:
+            for bit, name in REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in inside]), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(inside), "source": "nvml, 2 ms poll"}
 
 
 # ------------------------------------------------------------------------------------ oracle arm
@@ -232,6 +238,7 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
     launches = {"n": 0}
     rel_events = []
+    shift_events = []
 
     def relight_fn(Tc, band, Rc):
         e0 = torch.cuda.Event(enable_timing=True)
@@ -245,7 +252,12 @@ def run_ours(args, cfg):
     def step():
         """One pass of the hot path; returns this rank's result tensor (R, or R_full on rank 0)."""
         if rank == 0:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             hs.haar_shift_coeffs(light, shifts, 2, n if full_out else cfg.band_levels, out=shifted, workspace=ws)
+            e1.record(stream)
+            shift_events.append((e0, e1))
             launches["n"] += hs.last_launch_count()
         if world > 1:
             hsdist.broadcast_band(shifted)
@@ -259,17 +271,21 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     launches["n"] = 0
     rel_events.clear()
+    shift_events.clear()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(0.01)
+        clk.mark(True)
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -290,7 +306,7 @@ def run_ours(args, cfg):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(f"{cfg.name}:relight_b{B}")
+            traffic = json.load(fh).get(f"{cfg.name}:relight_b{B}") if (V == cfg.vertices and world == 1) else None
     except Exception:
         pass
 
@@ -340,6 +356,10 @@ def run_ours(args, cfg):
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes),
                          "avg_launch_ms": avg_ms, "share_of_step": sum(rel_ms) / args.steps / ms},
+            "shift_ms": (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events)) if shift_events else None,
+            "shift_frac_hbm": ((2 * B * F * N * N * 4 if full_out else B * F * (N * N + kf) * 4) /
+                               (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events) * 1e-3) / 1e9 / peak)
+            if shift_events else None,
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "e2e": e2e,

@@ -125,7 +125,8 @@ constexpr int kTileKF = 3;    // fine levels per tile: the tile root level is c 
 constexpr int kTileTC = 8;    // tile side at level c (cells)
 
 inline int coarse_level(int m) { return m > kTileKF ? m - kTileKF : 0; }
-inline long long ws_face_floats_2d(int n) {
+bool shift2d_uses_fp64(int log2n);        // field precision of the 2D tile kernel
+inline long long ws_face_floats_2d(int n) {  // elements of the field type per face
   int c = coarse_level(n);
   long long a = 3ll << (2 * c);
   long long b = c > 0 ? (3ll << (2 * (c - 1))) : 0;

@@ -107,8 +107,8 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces) {
   if (ndim != 2) return 0;
-  return align256((size_t)num_faces * sizeof(unsigned)) +
-         (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * sizeof(float);
+  const size_t esz = shift2d_uses_fp64(log2n) ? 8 : 4;
+  return align256((size_t)num_faces * sizeof(unsigned)) + (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * esz;
 }
 
 // in:  [num_faces / faces batches][faces][K]; out [num_faces][Kb]
@@ -139,7 +139,9 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     const long long g0 = b0 * faces;
     a.in = in + b0 * in_batch_stride;
     a.out = out + g0 * Kb;
-    a.ws = wsf ? wsf + g0 * wsface : nullptr;
+    a.ws = wsf ? reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) +
+                                         g0 * wsface * (shift2d_uses_fp64(n) ? 8 : 4))
+               : nullptr;
     a.counters = counters ? counters + g0 : nullptr;
     a.dev_fp = nullptr;
     a.in_batch_stride = in_batch_stride;

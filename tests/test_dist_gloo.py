@@ -1,0 +1,97 @@
+"""Multi-GPU plumbing on CPU (-m "not gpu"): world-size-2 (and 3) gloo process groups exercise the
+vertex-row sharding, the band broadcast and the chunked, overlapped radiance gather of
+paper_1705_07272_b200.dist.  The per-rank compute is an injected CPU double (a float64 matmul), not
+the oracle and not the product kernel; what is under test is that every rank's rows land at
+their global offsets in rank 0's radiance and that the result equals the unsharded one."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1705_07272_b200 import dist as hsdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _relight_double(T, band, R):
+    B = band.shape[0]
+    K = T.shape[1]
+    R.copy_((T.double() @ band.reshape(B, -1)[:, :K].double().T).float())
+
+
+def _worker(rank, world, port, V, F, kf, B, chunks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(7)
+        T_full = torch.randn(V, F * kf, generator=g)
+        band_full = torch.randn(B, F, kf, generator=g)
+        start, count = hsdist.shard_rows(V, world, rank)
+        T_local = T_full[start:start + count].contiguous()
+        band = band_full.clone() if rank == 0 else torch.zeros(B, F, kf)
+        hsdist.broadcast_band(band)
+        assert torch.equal(band, band_full)
+        R_full = torch.full((V, B), float("nan")) if rank == 0 else None
+        local, full = hsdist.relight_and_gather(T_local, band, V, _relight_double, R_full, chunks=chunks)
+        ref_local = torch.empty(count, B)
+        _relight_double(T_local, band_full, ref_local)
+        assert torch.equal(local, ref_local)
+        if rank == 0:
+            ref = torch.empty(V, B)
+            _relight_double(T_full, band_full, ref)
+            q.put(("ok", bool(torch.equal(full, ref)), float((full - ref).abs().max())))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), rank))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,V,chunks", [(2, 1001, 4), (2, 64, 1), (3, 1000, 3), (2, 5, 4)])
+def test_sharded_relight_gather_equals_unsharded(world, V, chunks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, V, 6, 16, 8, chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), msgs
+    oks = [m for m in msgs if m[0] == "ok"]
+    assert oks and oks[0][1], msgs
+
+
+def test_shard_rows_partition():
+    for V in [0, 1, 7, 1000, 1_000_000]:
+        for world in [1, 2, 3, 8]:
+            pieces = [hsdist.shard_rows(V, world, r) for r in range(world)]
+            assert sum(c for _, c in pieces) == V
+            pos = 0
+            for s, c in pieces:
+                assert s == pos
+                pos += c
+            assert max(c for _, c in pieces) - min(c for _, c in pieces) <= 1
+            assert hsdist.max_shard(V, world) == max(c for _, c in pieces)
+
+
+def test_chunk_bounds():
+    assert hsdist.chunk_bounds(10, 3) == [(0, 4), (4, 3), (7, 3)]
+    assert hsdist.chunk_bounds(2, 4) == [(0, 1), (1, 1)]
+    assert hsdist.chunk_bounds(0, 4) == []
+    with pytest.raises(ValueError):
+        hsdist.shard_rows(10, 2, 2)
