@@ -146,6 +146,7 @@ hs_status relight_vertices(const float* transfer, int64_t num_vertices, int face
 
 size_t relight_shifted_workspace_bytes(int64_t num_vertices, int faces, int log2n) {
   if (num_vertices < 1 || faces < 1 || log2n < 1 || log2n > HS_MAX_LOG2N) return 0;
+  if (relight_shifted_fused_supported(log2n)) return relight_shifted_fused_workspace_bytes(num_vertices, faces, log2n);
   const long long vc = num_vertices < kRelightChunk ? num_vertices : kRelightChunk;
   const long long nf = vc * faces;
   const size_t shift_ws = shift_workspace_bytes_impl(2, log2n, nf);
@@ -169,6 +170,12 @@ hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, 
   hs_status s = check_device();
   if (s != HS_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  if (relight_shifted_fused_supported(log2n)) {
+    s = launch_relight_shifted_fused(transfer, num_vertices, faces, light, log2n, vertex_shifts, radiance, workspace,
+                                     st);
+    g_last_launches = g_launches;
+    return s;
+  }
   const long long vc = num_vertices < kRelightChunk ? num_vertices : kRelightChunk;
   const long long K = (long long)faces << (2 * log2n);
   const size_t shift_ws = shift_workspace_bytes_impl(2, log2n, vc * faces);

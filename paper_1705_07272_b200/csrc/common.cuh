@@ -146,6 +146,10 @@ hs_status launch_relight(const float* T, long long V, int faces, int kface, cons
 size_t relight_tc_workspace_bytes(int faces, int kface, int batch);
 hs_status launch_rowdot(const float* T, const float* S, long long rows, long long K, float* R,
                         cudaStream_t st);
+bool relight_shifted_fused_supported(int log2n);
+size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n);
+hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, const float* light, int log2n,
+                                       const float* shifts, float* R, void* ws, cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
                                int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
 

@@ -1,0 +1,402 @@
+// Fused per-vertex shift + relight:  r_v = < S_{s_v} L , T_v >
+// (every pixel/vertex rotates by its own normal angles; the coarser levels
+// follow by the recursive h_s / h_t filters; plugged into the light-transport integral).
+// DESIGN.md §5.5.
+//
+// The shifted pyramid of a vertex is never materialised.  The three difference pipelines are
+// independent (X -> H, Y -> V, Z -> D), so the work is split into units (face f, field t):
+//   prep    : fields_kernel computes the full-resolution difference field F_n (t = X, Y or Z) of
+//             every face top-down from its detail coefficients (the shared light L, once per call),
+//             stored column-parity split;
+//   main    : one CTA holds one unit's field plane (N^2 floats) in shared memory and streams its
+//             share of the vertices.  Per vertex: the fused shift + first bottom-up stencil
+//             (level n -> n-1) with a register sliding window down each thread's column strip,
+//             the [1,1] x [1,2,1] bottom-up to level 0, and the running dot of every shifted
+//             detail coefficient of type t with T_v; one partial sum per (vertex, unit);
+//   finish  : r_v = sum over units of the partials + sum_f T_v[f][0] L_f[0] (the scaling
+//             coefficient is shift invariant).
+// Every shift is processed at the finest level (integer shifts have phi = 0), which is exact.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace hs {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// ------------------------------------------------------------------------------- prep
+// fields[f][t][parity][r][c/2] = F_n[r][c] for t in {X, Y, Z}; one CTA per face, top-down over the
+// whole (periodic) grid, level by level, ping-ponging through the scratch area.
+__global__ void __launch_bounds__(kThreads) fields_kernel(const float* __restrict__ light, int n,
+                                                          float* __restrict__ fields, float* __restrict__ scratch) {
+  const int f = blockIdx.x;
+  const int N = 1 << n;
+  const long long NN = (long long)N * N;
+  const float* in = light + (long long)f * NN;
+  float* buf[2] = {scratch + (long long)f * 6 * NN, scratch + (long long)f * 6 * NN + 3 * NN};
+  // level 0 fields are 0; level l+1 from level l
+  for (int l = 0; l < n; ++l) {
+    const int g = 1 << l, G = 2 * g;
+    const float asc = pow2f(l);
+    const float* cur = buf[l & 1];
+    const bool last = (l + 1 == n);
+    float* nxt = buf[(l + 1) & 1];
+    for (int idx = threadIdx.x; idx < g * g; idx += blockDim.x) {
+      const int i = idx >> l, j = idx & (g - 1);
+      float d[2][2][2][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int ii = (i + u) & (g - 1), jj = (j + v) & (g - 1);
+          const long long o = (long long)ii * g + jj;
+          const float H = __ldg(in + (long long)g * g * 1 + o) * asc;
+          const float V = __ldg(in + (long long)g * g * 2 + o) * asc;
+          const float D = __ldg(in + (long long)g * g * 3 + o) * asc;
+          d[u][v][0][0] = H + V + D;
+          d[u][v][0][1] = -H + V - D;
+          d[u][v][1][0] = H - V - D;
+          d[u][v][1][1] = -H - V + D;
+        }
+      float Xl = 0.f, Yl = 0.f, Zl = 0.f;
+      if (l > 0) {
+        Xl = __ldcg(cur + idx);
+        Yl = __ldcg(cur + g * g + idx);
+        Zl = __ldcg(cur + 2 * g * g + idx);
+      }
+      float cx[2][2], cy[2][2], cz[2][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        cx[a][0] = d[0][0][a][0] - d[0][0][a][1];
+        cx[a][1] = Xl + d[0][0][a][1] - d[0][1][a][0];
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        cy[0][b] = d[0][0][0][b] - d[0][0][1][b];
+        cy[1][b] = Yl + d[0][0][1][b] - d[1][0][0][b];
+      }
+      cz[0][0] = d[0][0][0][0] - d[0][0][0][1] - d[0][0][1][0] + d[0][0][1][1];
+      cz[0][1] = d[0][0][0][1] - d[0][0][1][1] - d[0][1][0][0] + d[0][1][1][0];
+      cz[1][0] = d[0][0][1][0] - d[0][0][1][1] - d[1][0][0][0] + d[1][0][0][1];
+      cz[1][1] = Zl + d[0][0][1][1] - d[0][1][1][0] - d[1][0][0][1] + d[1][1][0][0];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int r = 2 * i + a, c = 2 * j + b;
+          if (!last) {
+            const int o = r * G + c;
+            nxt[o] = cx[a][b];
+            nxt[G * G + o] = cy[a][b];
+            nxt[2 * G * G + o] = cz[a][b];
+          } else {
+            // final layout: [f][t][parity][r][c/2]
+            float* base = fields + (long long)f * 3 * NN;
+            const long long o = (long long)(c & 1) * (NN / 2) + (long long)r * (N / 2) + (c >> 1);
+            base[o] = cx[a][b];
+            base[NN + o] = cy[a][b];
+            base[2 * NN + o] = cz[a][b];
+          }
+        }
+    }
+    __syncthreads();
+    __threadfence_block();
+  }
+}
+
+// ------------------------------------------------------------------------------- main
+template <int LOG2N>
+struct Geo {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int G = N / 2;                  // level n-1 side
+  static constexpr int NS = kThreads / G;          // row strips at level n-1
+  static constexpr int RS = G / NS;                // output rows per strip
+  static constexpr int PADR = 2 * RS + 4;          // wrapped rows appended to the field plane
+  static constexpr int HP = N / 2;                 // half-row length (parity split)
+  static constexpr int PLANE = (N + PADR) * HP;    // one parity plane, padded
+  static constexpr int SMEM = (2 * PLANE + G * G + (G / 2) * (G / 2) + 64) * 4;
+  static_assert(kThreads % G == 0 && G % NS == 0, "geometry");
+  // transfer values a thread dots at bottom-up level lev (cells tid, tid + 256, ...)
+  static constexpr int cpt(int lev) { return (1 << (2 * lev)) > kThreads ? (1 << (2 * lev)) / kThreads : 1; }
+  static constexpr int tb_off(int lev) {
+    int o = 0;
+    for (int l = 0; l < lev; ++l) o += cpt(l);
+    return o;
+  }
+  static constexpr int NTB = tb_off(LOG2N - 1);  // levels 0 .. n-2
+};
+
+// Per-vertex shift classification, once per call (fp64, the same split as the host path).
+__global__ void vertex_params_kernel(const float* __restrict__ shifts, long long V, int N, int4* __restrict__ out) {
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  int qy, qx;
+  double py, px;
+  split_shift((double)shifts[2 * v], N, &qy, &py);
+  split_shift((double)shifts[2 * v + 1], N, &qx, &px);
+  out[v] = make_int4(qy, qx, __float_as_int((float)py), __float_as_int((float)px));
+}
+
+// One bottom-up level LEV (and, recursively, all coarser ones): shifted fields of level LEV from
+// level LEV+1 (periodic), the detail output dotted with the prefetched transfer values tb.
+template <int LOG2N, int FLD, int LEV, int NTB>
+__device__ __forceinline__ void bottom_up(const float* src, float* dst, const float (&tb)[NTB], float& acc) {
+  if constexpr (LEV >= 0) {
+    using Gm = Geo<LOG2N>;
+    constexpr int g = 1 << LEV, Gs = 2 * g;
+    const float osc = pow2f(-LEV);
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < Gm::cpt(LEV); ++k) {
+      const int idx = tid + k * kThreads;
+      if (idx < g * g) {
+        const int i = idx >> LEV, jj = idx & (g - 1);
+        const float* p0 = src + (2 * i) * Gs;
+        const float* p1 = p0 + Gs;
+        const float* p2 = src + ((2 * i + 2) & (Gs - 1)) * Gs;
+        const int c0 = 2 * jj, c1 = 2 * jj + 1, c2 = (2 * jj + 2) & (Gs - 1);
+        float fv, dv;
+        if (FLD == 0) {
+          fv = 0.25f * (p0[c0] + 2.f * p0[c1] + p0[c2] + p1[c0] + 2.f * p1[c1] + p1[c2]);
+          dv = 0.25f * (p0[c0] + p1[c0]);
+        } else if (FLD == 1) {
+          fv = 0.25f * (p0[c0] + 2.f * p1[c0] + p2[c0] + p0[c1] + 2.f * p1[c1] + p2[c1]);
+          dv = 0.25f * (p0[c0] + p0[c1]);
+        } else {
+          fv = 0.25f * ((p0[c0] + 2.f * p0[c1] + p0[c2]) + 2.f * (p1[c0] + 2.f * p1[c1] + p1[c2]) +
+                        (p2[c0] + 2.f * p2[c1] + p2[c2]));
+          dv = 0.25f * p0[c0];
+        }
+        dst[idx] = fv;
+        acc = fmaf(dv * osc, tb[Gm::tb_off(LEV) + k], acc);
+      }
+    }
+    __syncthreads();
+    bottom_up<LOG2N, FLD, LEV - 1, NTB>(dst, const_cast<float*>(src), tb, acc);
+  }
+}
+
+// One (face f, field FLD) unit over the vertex range [v0, v1).  FLD: 0 = X -> H, 1 = Y -> V,
+// 2 = Z -> D.  The field plane sits in shared memory parity split and padded with PADR wrapped
+// rows, so every tap of a thread's strip is an immediate offset from four per-vertex bases.
+template <int LOG2N, int FLD>
+__device__ __forceinline__ void unit_body(float* sm, const float* __restrict__ T, int faces, int f,
+                                          const int4* __restrict__ vparams, float* __restrict__ partial, int unit,
+                                          int units, long long v0, long long v1) {
+  using Gm = Geo<LOG2N>;
+  constexpr int N = Gm::N, G = Gm::G, RS = Gm::RS, HP = Gm::HP, PLANE = Gm::PLANE;
+  constexpr int n = LOG2N;
+  constexpr int NTAP = (FLD == 1) ? 3 : 4;
+  float* S1 = sm + 2 * PLANE;       // shifted field at level n-1 (G x G)
+  float* S2 = S1 + G * G;           // level n-2
+  float* red = S2 + (G / 2) * (G / 2);
+  const long long NN = (long long)N * N;
+  const long long Kt = (long long)faces * NN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j = tid % G;            // level n-1 column owned by this thread
+  const int i0 = (tid / G) * RS;    // first output row of this thread's strip
+  constexpr int lvl1 = n - 1;
+  const float osc1 = pow2f(-lvl1);
+
+#define HS_LOAD_T(VV, TV, TB, PR)                                                        \
+  if ((VV) < v1) {                                                                      \
+    PR = __ldg(vparams + (VV));                                                         \
+    const float* Tv_ = T + (VV) * Kt + (long long)f * NN;                               \
+    const float* Trow_ = Tv_ + ((long long)(1 + FLD) << (2 * lvl1)) + j;                \
+    _Pragma("unroll") for (int r_ = 0; r_ < RS; ++r_) TV[r_] = __ldg(Trow_ + (i0 + r_) * G); \
+    _Pragma("unroll") for (int lev_ = 0; lev_ <= n - 2; ++lev_) {                       \
+      const float* Tl_ = Tv_ + ((long long)(1 + FLD) << (2 * lev_));                    \
+      _Pragma("unroll") for (int k_ = 0; k_ < Gm::cpt(lev_); ++k_) {                    \
+        const int idx_ = tid + k_ * kThreads;                                           \
+        TB[Gm::tb_off(lev_) + k_] = (idx_ < (1 << (2 * lev_))) ? __ldg(Tl_ + idx_) : 0.f; \
+      }                                                                                 \
+    }                                                                                   \
+  }
+  constexpr int NTBX = Gm::NTB > 0 ? Gm::NTB : 1;
+  float tv[RS], tb[NTBX];
+  int4 pr = make_int4(0, 0, 0, 0);
+  HS_LOAD_T(v0, tv, tb, pr);
+  for (long long v = v0; v < v1; ++v) {
+    float tvn[RS], tbn[NTBX];
+    int4 prn = pr;
+    HS_LOAD_T(v + 1, tvn, tbn, prn);  // software pipeline: next vertex's loads in flight
+    const int qy = pr.x, qx = pr.y;
+    const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
+    float acc = 0.f;
+    // ---- level n -> n-1: fused shift + first bottom-up, sliding down this thread's rows.
+    // window row u (0-based) = level-n row ((2 i0 - qy - 1) & (N-1)) + u, no wrap (padded plane);
+    // column tap v = -1..2 at level n: c = 2j - qx + v (periodic), parity split
+    const int rs = (2 * i0 - qy - 1) & (N - 1);
+    const float* base[NTAP];
+#pragma unroll
+    for (int vv = 0; vv < NTAP; ++vv) {
+      const int c = (2 * j - qx + vv - 1) & (N - 1);
+      base[vv] = sm + (c & 1) * PLANE + rs * HP + (c >> 1);
+    }
+    // horizontal filters: field tent [w1, w0+2w1, 2w0+w1, w0] (X, Z) or [w1, 1, w0] (Y);
+    // detail [w1, w0] (X, Z) or the Y field filter itself
+    const float ta = wx1, tb0 = wx0 + 2.f * wx1, tb1 = 2.f * wx0 + wx1, tc = wx0;
+    float hA[RS * 2 + 2], hB[RS * 2 + 2];
+#pragma unroll
+    for (int u = 0; u < 2 * RS + 2; ++u) {
+      const float x_1 = base[0][u * HP], x0 = base[1][u * HP], x1 = base[2][u * HP];
+      if (FLD == 1) {
+        hA[u] = fmaf(wx1, x_1, fmaf(wx0, x1, x0));
+        hB[u] = hA[u];
+      } else {
+        const float x2 = base[NTAP - 1][u * HP];
+        hA[u] = fmaf(ta, x_1, fmaf(tb0, x0, fmaf(tb1, x1, tc * x2)));
+        hB[u] = fmaf(wx1, x_1, wx0 * x0);
+      }
+    }
+    const float ua = wy1, ub0 = wy0 + 2.f * wy1, ub1 = 2.f * wy0 + wy1, uc = wy0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const int u = 2 * r;  // window rows u .. u+3 <-> taps -1..2 of output row i0 + r
+      float fld, det;
+      if (FLD == 0) {  // X: rows [w1, 1, w0] on taps -1..1, detail rows the same
+        fld = 0.25f * fmaf(wy1, hA[u], fmaf(wy0, hA[u + 2], hA[u + 1]));
+        det = 0.25f * fmaf(wy1, hB[u], fmaf(wy0, hB[u + 2], hB[u + 1]));
+      } else {         // Y, Z: rows tent on taps -1..2; detail rows [w1, w0] on taps -1, 0
+        fld = 0.25f * fmaf(ua, hA[u], fmaf(ub0, hA[u + 1], fmaf(ub1, hA[u + 2], uc * hA[u + 3])));
+        det = 0.25f * fmaf(wy1, hB[u], wy0 * hB[u + 1]);
+      }
+      S1[(i0 + r) * G + j] = fld;
+      acc = fmaf(det * osc1, tv[r], acc);
+    }
+    __syncthreads();
+    // ---- bottom-up n-2 .. 0 (periodic), ping-pong S1 -> S2 -> S1 ... (compile-time levels)
+    bottom_up<LOG2N, FLD, LOG2N - 2>(S1, S2, tb, acc);
+    // ---- CTA reduction of the partial sum (fixed order -> deterministic)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+      partial[v * units + unit] = s;
+    }
+#pragma unroll
+    for (int r = 0; r < RS; ++r) tv[r] = tvn[r];
+#pragma unroll
+    for (int k = 0; k < Gm::NTB; ++k) tb[k] = tbn[k];
+    pr = prn;
+  }
+#undef HS_LOAD_T
+}
+
+template <int LOG2N>
+__global__ void __launch_bounds__(kThreads, 2)
+    relight_shifted_unit_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ fields,
+                                const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
+  using Gm = Geo<LOG2N>;
+  constexpr int N = Gm::N, HP = Gm::HP, PLANE = Gm::PLANE, PADR = Gm::PADR;
+  extern __shared__ __align__(16) float sm[];
+  const int units = 3 * faces;
+  const int unit = blockIdx.x % units;
+  const int split = blockIdx.x / units;
+  const int f = unit / 3, t = unit - 3 * (unit / 3);
+  const long long NN = (long long)N * N;
+  // field plane -> smem, parity split [2][N + PADR][N/2], rows N.. = rows 0.. (periodic padding)
+  {
+    const float* src = fields + ((long long)f * 3 + t) * NN;
+    for (int idx = threadIdx.x; idx < 2 * (N + PADR) * HP; idx += kThreads) {
+      const int par = idx / PLANE, rem = idx - par * PLANE;
+      const int r = rem / HP, c = rem - r * HP;
+      sm[idx] = __ldg(src + (long long)par * (NN / 2) + (r & (N - 1)) * HP + c);
+    }
+  }
+  __syncthreads();
+  const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
+  if (t == 0) unit_body<LOG2N, 0>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else if (t == 1) unit_body<LOG2N, 1>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else unit_body<LOG2N, 2>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
+}
+
+__global__ void relight_shifted_finish_kernel(const float* __restrict__ partial, const float* __restrict__ T,
+                                              const float* __restrict__ light, long long V, int faces, int n,
+                                              float* __restrict__ R) {
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int units = 3 * faces;
+  const long long NN = 1ll << (2 * n);
+  float s = 0.f;
+  for (int u = 0; u < units; ++u) s += partial[v * units + u];
+  for (int f = 0; f < faces; ++f) s = fmaf(__ldg(T + v * faces * NN + f * NN), __ldg(light + f * NN), s);
+  R[v] = s;
+}
+
+int num_sms_rs() {
+  static int n = 0;
+  if (!n) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int LOG2N>
+hs_status launch_unit(const float* T, long long V, int faces, const float* fields, const int4* shifts,
+                      float* partial, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    HS_CHECK_CUDA(cudaFuncSetAttribute(relight_shifted_unit_kernel<LOG2N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<LOG2N>::SMEM),
+                  "cudaFuncSetAttribute(relight_shifted_unit_kernel)");
+    attr = true;
+  }
+  const int units = 3 * faces;
+  int per_sm = 227 * 1024 / (Geo<LOG2N>::SMEM + 1024);
+  if (per_sm > 2) per_sm = 2;
+  if (per_sm < 1) per_sm = 1;
+  int nsplit = (num_sms_rs() * per_sm) / units;
+  if (nsplit < 1) nsplit = 1;
+  if (nsplit > V) nsplit = (int)V;
+  relight_shifted_unit_kernel<LOG2N><<<units * nsplit, kThreads, Geo<LOG2N>::SMEM, st>>>(T, V, faces, fields, shifts,
+                                                                                           partial, nsplit);
+  HS_CHECK_LAUNCH("relight_shifted_unit_kernel");
+  return HS_OK;
+}
+
+}  // namespace
+
+bool relight_shifted_fused_supported(int log2n) { return log2n >= 5 && log2n <= 7; }
+
+size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n) {
+  const size_t NN = (size_t)1 << (2 * log2n);
+  return (size_t)faces * 3 * NN * 4 /*fields*/ + (size_t)faces * 6 * NN * 4 /*scratch*/ +
+         (size_t)V * 3 * faces * 4 /*partials*/ + (size_t)V * 16 /*vertex params*/ + 512;
+}
+
+hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, const float* light, int log2n,
+                                       const float* shifts, float* R, void* ws, cudaStream_t st) {
+  const size_t NN = (size_t)1 << (2 * log2n);
+  float* fields = reinterpret_cast<float*>(ws);
+  float* scratch = fields + (size_t)faces * 3 * NN;
+  float* partial = scratch + (size_t)faces * 6 * NN;
+  int4* vp = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(partial + (size_t)V * 3 * faces) + 255) & ~uintptr_t(255));
+  fields_kernel<<<faces, kThreads, 0, st>>>(light, log2n, fields, scratch);
+  HS_CHECK_LAUNCH("fields_kernel");
+  vertex_params_kernel<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(shifts, V, 1 << log2n, vp);
+  HS_CHECK_LAUNCH("vertex_params_kernel");
+  hs_status s = HS_OK;
+  switch (log2n) {
+    case 5: s = launch_unit<5>(T, V, faces, fields, vp, partial, st); break;
+    case 6: s = launch_unit<6>(T, V, faces, fields, vp, partial, st); break;
+    case 7: s = launch_unit<7>(T, V, faces, fields, vp, partial, st); break;
+    default: return HS_ERR_UNSUPPORTED;
+  }
+  if (s != HS_OK) return s;
+  relight_shifted_finish_kernel<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(partial, T, light, V, faces, log2n, R);
+  HS_CHECK_LAUNCH("relight_shifted_finish_kernel");
+  return HS_OK;
+}
+
+}  // namespace hs

@@ -52,7 +52,8 @@ def test_workspace_sizes(lib):
     assert w == ((384 * 4 + 255) // 256) * 256 + 384 * (3 * 1024 + 3 * 256) * 4
     assert lib.haar_shift_workspace_bytes(2, 0, 1, 1) == 0
     assert lib.haar_shift_workspace_bytes(2, 13, 1, 1) == 0
-    assert lib.relight_shifted_workspace_bytes(100000, 6, 7) > 128 * 6 * 16384 * 4
+    assert lib.relight_shifted_workspace_bytes(100000, 6, 7) >= 3 * 6 * 16384 * 4 + 100000 * 18 * 4  # fused: fields + partials
+    assert lib.relight_shifted_workspace_bytes(100, 6, 8) > 100 * 6 * 65536 * 4                   # N > 128: chunked
 
 
 FAKE = 1 << 20  # an aligned, never-dereferenced "device" address
