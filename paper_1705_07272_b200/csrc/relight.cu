@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) relight_gemv_kernel(const float* __restri
       const long long row = (r0 + r < V) ? r0 + r : V - 1;
       Tr[r] = T + row * (long long)K;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int k = lane * 4; k < K; k += 128) {
       float4 t[RPW];
 #pragma unroll
@@ -191,10 +191,10 @@ int sm_count() {
 template <int B>
 hs_status gemv(const float* T, long long V, int K, int kshift, const float* L, long long lstride,
                long long lbatch, float* R, cudaStream_t st) {
-  constexpr int RPW = (B <= 2) ? 4 : 2;
+  constexpr int RPW = (B <= 4) ? 2 : 1;  // small tasks: one balanced wave of warps per SM
   const long long groups = (V + RPW - 1) / RPW;
   long long blocks = (groups + 7) / 8;
-  const long long cap = (long long)sm_count() * 8;
+  const long long cap = (long long)sm_count() * 64;  // grid-stride beyond 64 blocks per SM
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   relight_gemv_kernel<B, RPW><<<(unsigned)blocks, 256, 0, st>>>(T, V, K, kshift, L, lstride, lbatch, R);

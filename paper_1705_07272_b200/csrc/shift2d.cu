@@ -70,6 +70,8 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // Exact 2^e for |e| < 127 (no libm call).
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
@@ -146,125 +148,163 @@ __device__ void coarse_finish(const FT* src0, FT* b0, FT* b1, int c, float* __re
   }
 }
 
-template <typename FT>
-__global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_constant__ ShiftArgs args) {
-  using S = Smem<FT>;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int sR[2][2][HS_MAX_LOG2N + 1];  // [axis][start|size][level]
-  __shared__ int sDoff[HS_MAX_LOG2N + 2];      // detail window offset per level (floats)
-  __shared__ int sLast;
+// ------------------------------------------------------------------------------------------
+// Compile-time tile geometry for K fine levels below a TC x TC tile at the tile-root level c.
+// d = m - l counts levels above the working level m.  Window sides are maxima (the actual
+// windows, whose starts are runtime, fit inside; extra cells are computed from valid periodic
+// data and never written out).
+template <int K, int TC>
+struct TGeo {
+  static constexpr int FW = (TC + 1) << K;                    // level-m field window
+  static constexpr int P(int d) {                              // parent window at level m-d
+    int s = FW;
+    for (int i = 0; i < d; ++i) s = s / 2 + 1;
+    return s;
+  }
+  static constexpr int P1 = P(1);                              // parents at level m-1
+  static constexpr int CH = 2 * P1;                            // level-m children side
+  static constexpr int HC = P1;                                // parity half row
+  static constexpr int CB = 2 * P(2);                          // level m-1 field side
+  static constexpr int SN(int e) { return ((TC + 1) << e) - 1; }  // shifted window at c+e
+  static constexpr int SN1 = SN(K - 1);
+  static constexpr int NSTRIP = (kThreads / SN1 < SN1) ? kThreads / SN1 : SN1;
+  static constexpr int RSS = (SN1 + NSTRIP - 1) / NSTRIP;      // fused-stencil rows per strip
+  static constexpr int CHR = CH + 2 * (NSTRIP * RSS - SN1) + 4; // child plane rows incl. spare
+  static constexpr int DETW(int d) { return P(d) + 1; }
+  static constexpr int DET_MAX = [] {
+    int o = 0;
+    for (int d = 1; d <= HS_MAX_LOG2N; ++d) o += 3 * DETW(d) * DETW(d);
+    return o;
+  }();
+  static constexpr int ANC_MAX = 2 * P(3) > 2 * P(4) ? 2 * P(3) : 2 * P(4);  // level <= m-2 side
+};
 
-  const int g = blockIdx.y;  // face within this launch
-  const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
+template <typename FT, int K, int TC>
+struct TSmem {
+  using G = TGeo<K, TC>;
+  static constexpr int DET = 0;                                                      // float
+  static constexpr int B1 = (DET + G::DET_MAX * 4 + 15) / 16 * 16;                   // FT[3][CB^2]
+  static constexpr int CHILD = B1 + 3 * G::CB * G::CB * (int)sizeof(FT);             // FT[3][2][CHR][HC]
+  static constexpr int BYTES = CHILD + 3 * 2 * G::CHR * G::HC * (int)sizeof(FT);
+  static_assert(3 * G::ANC_MAX * G::ANC_MAX <= 3 * 2 * G::CHR * G::HC, "ancestor fields alias the child planes");
+  static_assert(3 * G::SN1 * G::SN1 <= 3 * G::CB * G::CB, "shifted m-1 window aliases B1");
+};
+
+template <typename FT, int K, int TC>
+__device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* smem, const FaceParam& P, int g,
+                                          int m, int c, int i0, int j0, int tpr, int (*sR)[2][HS_MAX_LOG2N + 1],
+                                          int* sDoff, int* sLast) {
+  using G = TGeo<K, TC>;
+  using S = TSmem<FT, K, TC>;
+  constexpr int CB = G::CB, CH = G::CH, HC = G::HC, CHR = G::CHR, SN1 = G::SN1;
+  constexpr int PLANE_C = CHR * HC;  // one parity plane of one field's children
   const int n = args.log2n;
-  const int m = P.m;
-  if (m == 0) return;  // identity: handled by permute_kernel
-  const int c = m > KF ? m - KF : 0;
-  const int k = m - c;
-  const int tc = (1 << c) < TC ? (1 << c) : TC;
-  const int tpr = (1 << c) / tc;  // tiles per row
-  if ((int)blockIdx.x >= tpr * tpr) return;
-  const int i0 = (blockIdx.x / tpr) * tc;
-  const int j0 = (blockIdx.x % tpr) * tc;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in =
       args.in + (long long)b * args.in_batch_stride + (long long)f * ((long long)1 << (2 * n));
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const int band = args.band;
   const int tid = threadIdx.x;
-
   float* sDet = reinterpret_cast<float*>(smem + S::DET);
-  FT* sFB = reinterpret_cast<FT*>(smem + S::FB);
-  FT* sFS = reinterpret_cast<FT*>(smem + S::FS);
-  FT* sBig = reinterpret_cast<FT*>(smem + S::BIG);
+  FT* sB1 = reinterpret_cast<FT*>(smem + S::B1);
+  FT* sCh = reinterpret_cast<FT*>(smem + S::CHILD);
 
-  // ---- regions: level-m field window F_m = [2^k i0 - Q - 1, +2^k (tc+1)); P_l = parents of P_{l+1}
+  // ---- window starts: level-m window [2^K i0 - Q - 1, + FW); level m-d starts at floor(s/2^d)
   if (tid < 2) {
     const int Q = tid == 0 ? P.Qy : P.Qx;
     const int o = tid == 0 ? i0 : j0;
-    int s = (o << k) - Q - 1;
-    int e = s + ((tc + 1) << k) - 1;
+    int s = (o << K) - Q - 1;
     for (int l = m - 1; l >= 0; --l) {
-      s >>= 1;  // arithmetic shift = floor division for negatives
-      e >>= 1;
+      s >>= 1;
       sR[tid][0][l] = s;
-      sR[tid][1][l] = e - s + 1;
     }
   }
-  __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // detail window of level l = m-d has side P(d)+1 (compile-time table)
     int off = 0;
-    for (int l = 0; l < m; ++l) {
+    for (int l = m - 1; l >= 0; --l) {
       sDoff[l] = off;
-      off += 3 * (sR[0][1][l] + 1) * (sR[1][1][l] + 1);
+      const int w = G::DETW(m - l);
+      off += 3 * w * w;
+      sR[0][1][l] = G::P(m - l);
+      sR[1][1][l] = G::P(m - l);
     }
     sDoff[m] = off;
   }
   __syncthreads();
 
-  // ---- all detail windows (parents + 1 neighbour row/column) of levels 0..m-1 in one round trip:
-  //      one flat loop over every level's [3][yn+1][xn+1] window; a thread's flat index only grows,
-  //      so its level pointer only moves forward; divisions by the (small) window sizes use an
-  //      exact float reciprocal: floor((e + 0.5) / n) is exact for e < 2^16, n < 2^8.
+  // ---- detail windows in two cp.async groups (flat loops, level pointer monotone per thread):
+  //      group A = ancestors' windows (levels <= m-3), group B = the large windows of levels
+  //      m-2 and m-1; the ancestors' top-down runs while group B is still in flight.
   {
-    const int total = sDoff[m];
-    int l = -1, lend = 0, lbeg = 0, per = 1, xn = 1, ys = 0, xs = 0, mask = 0;
-    float inv_per = 1.f, inv_xn = 1.f;
-    for (int e = tid; e < total; e += kThreads) {
-      while (e >= lend) {  // advance to the level holding e (monotone per thread)
-        ++l;
-        lbeg = sDoff[l];
-        lend = sDoff[l + 1];
-        xn = sR[1][1][l] + 1;
-        per = (sR[0][1][l] + 1) * xn;
-        ys = sR[0][0][l];
-        xs = sR[1][0][l];
-        mask = (1 << l) - 1;
-        inv_per = inv_small(per);
-        inv_xn = inv_small(xn);
+    auto load_range = [&](int lhi, int llo) {  // levels lhi down to llo (stored m-1 first)
+      if (lhi < llo) return;
+      const int beg = sDoff[lhi], total = sDoff[llo] + 3 * (sR[0][1][llo] + 1) * (sR[0][1][llo] + 1);
+      int l = lhi + 1, lbeg = 0, lend = beg, w = 1, per = 1, ys = 0, xs = 0, mask = 0;
+      float inv_per = 1.f, inv_w = 1.f;
+      for (int e = beg + tid; e < total; e += kThreads) {
+        while (e >= lend) {
+          --l;
+          lbeg = sDoff[l];
+          w = sR[0][1][l] + 1;
+          per = w * w;
+          lend = lbeg + 3 * per;
+          ys = sR[0][0][l];
+          xs = sR[1][0][l];
+          mask = (1 << l) - 1;
+          inv_per = inv_small(per);
+          inv_w = inv_small(w);
+        }
+        const int loc = e - lbeg;
+        const int t = div_small(loc, inv_per);
+        const int rem = loc - t * per;
+        const int a = div_small(rem, inv_w);
+        const int bb = rem - a * w;
+        cp_async4(sDet + e, in + (((1 + t) << (2 * l)) + (((ys + a) & mask) << l) + ((xs + bb) & mask)));
       }
-      const int loc = e - lbeg;
-      const int t = div_small(loc, inv_per);
-      const int rem = loc - t * per;
-      const int a = div_small(rem, inv_xn);
-      const int bb = rem - a * xn;
-      cp_async4(sDet + e, in + (((1 + t) << (2 * l)) + (((ys + a) & mask) << l) + ((xs + bb) & mask)));
-    }
+    };
+    load_range(m - 3, 0);                      // group A
+    cp_async_commit();
+    load_range(m - 1, m >= 2 ? m - 2 : m - 1); // group B
+    cp_async_commit();
+    cp_async_wait_group1();                    // A complete, B may be in flight
   }
-  cp_async_wait_all();
   __syncthreads();
 
-  // ---- (1) top-down l -> l+1 for l = 0 .. m-2, all three fields; level m-1 lands in sFB
-  for (int l = 0; l + 1 < m; ++l) {
-    const int ys = sR[0][0][l], yn = sR[0][1][l], xs = sR[1][0][l], xn = sR[1][1][l];
-    const int dn = xn + 1, dplane = (yn + 1) * dn;
+  // ---- (1) ancestors top-down: fields of levels 1 .. m-1 (level m-1 -> sB1, others alias sCh)
+  auto ancestor_level = [&](int l) {
+    const int d = m - l;                      // parent window at level l: P(d)
+    const int pw = sR[0][1][l];
+    const int ys = sR[0][0][l], xs = sR[1][0][l];
+    const int dw = pw + 1, dplane = dw * dw;
     const float* dt = sDet + sDoff[l];
     const FT asc = FT(pow2f(l));
-    const bool dst_big = ((m - 2 - l) & 1) == 0;  // child level l+1; level m-1 -> big buffer
-    FT* cf = dst_big ? sFB : sFS;
-    const int cplane = dst_big ? CB * CB : CSM * CSM;
-    const FT* pf = dst_big ? sFS : sFB;
-    const int pplane = dst_big ? CSM * CSM : CB * CB;
+    const bool to_b1 = (l + 1 == m - 1);
+    // children at level l+1 land in: level m-1 -> sB1 (side CB); else alternate halves of sCh
+    FT* cf = to_b1 ? sB1 : sCh + ((((m - 2 - l) & 1) == 0) ? 0 : 3 * G::ANC_MAX * G::ANC_MAX);
+    const int cside = 2 * pw;
+    const int cplane = to_b1 ? CB * CB : G::ANC_MAX * G::ANC_MAX;
+    const FT* pf = sCh + ((((m - 2 - l) & 1) == 0) ? 3 * G::ANC_MAX * G::ANC_MAX : 0);
+    const int pplane = G::ANC_MAX * G::ANC_MAX;
     int pstride = 0, poy = 0, pox = 0;
     if (l > 0) {
-      pstride = 2 * sR[1][1][l - 1];
+      pstride = 2 * sR[0][1][l - 1];
       poy = ys - 2 * sR[0][0][l - 1];
       pox = xs - 2 * sR[1][0][l - 1];
     }
-    const int cstride = 2 * xn;
-    for (Walk2 w(yn * xn, xn); w.idx < yn * xn; w.next()) {
-      const int pi = w.r, pj = w.c;
-      FT d[2][2][2][2];  // [u][w][a][b] = delta_ab at cell (i+u, j+w)
+    const float inv_pw = inv_small(pw);
+    for (int idx = tid; idx < pw * pw; idx += kThreads) {
+      const int pi = div_small(idx, inv_pw), pj = idx - pi * pw;
+      FT dd[2][2][2][2];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int o = (pi + u) * dn + (pj + v);
+          const int o = (pi + u) * dw + (pj + v);
           const FT H = FT(dt[o]) * asc, V = FT(dt[dplane + o]) * asc, D = FT(dt[2 * dplane + o]) * asc;
-          d[u][v][0][0] = H + V + D;
-          d[u][v][0][1] = -H + V - D;
-          d[u][v][1][0] = H - V - D;
-          d[u][v][1][1] = -H - V + D;
+          dd[u][v][0][0] = H + V + D;
+          dd[u][v][0][1] = -H + V - D;
+          dd[u][v][1][0] = H - V - D;
+          dd[u][v][1][1] = -H - V + D;
         }
       FT Xl = FT(0), Yl = FT(0), Zl = FT(0);
       if (l > 0) {
@@ -273,164 +313,174 @@ __global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_con
         Yl = pf[pplane + po];
         Zl = pf[2 * pplane + po];
       }
-      const int co = (2 * pi) * cstride + 2 * pj;
+      const int co = (2 * pi) * cside + 2 * pj;
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
-        cf[co + a * cstride + 0] = d[0][0][a][0] - d[0][0][a][1];
-        cf[co + a * cstride + 1] = Xl + d[0][0][a][1] - d[0][1][a][0];
+        cf[co + a * cside + 0] = dd[0][0][a][0] - dd[0][0][a][1];
+        cf[co + a * cside + 1] = Xl + dd[0][0][a][1] - dd[0][1][a][0];
       }
 #pragma unroll
       for (int bq = 0; bq < 2; ++bq) {
-        cf[cplane + co + bq] = d[0][0][0][bq] - d[0][0][1][bq];
-        cf[cplane + co + cstride + bq] = Yl + d[0][0][1][bq] - d[1][0][0][bq];
+        cf[cplane + co + bq] = dd[0][0][0][bq] - dd[0][0][1][bq];
+        cf[cplane + co + cside + bq] = Yl + dd[0][0][1][bq] - dd[1][0][0][bq];
       }
-      cf[2 * cplane + co] = d[0][0][0][0] - d[0][0][0][1] - d[0][0][1][0] + d[0][0][1][1];  // = 4 D^
-      cf[2 * cplane + co + 1] = d[0][0][0][1] - d[0][0][1][1] - d[0][1][0][0] + d[0][1][1][0];
-      cf[2 * cplane + co + cstride] = d[0][0][1][0] - d[0][0][1][1] - d[1][0][0][0] + d[1][0][0][1];
-      cf[2 * cplane + co + cstride + 1] = Zl + d[0][0][1][1] - d[0][1][1][0] - d[1][0][0][1] + d[1][1][0][0];
+      cf[2 * cplane + co] = dd[0][0][0][0] - dd[0][0][0][1] - dd[0][0][1][0] + dd[0][0][1][1];
+      cf[2 * cplane + co + 1] = dd[0][0][0][1] - dd[0][0][1][1] - dd[0][1][0][0] + dd[0][1][1][0];
+      cf[2 * cplane + co + cside] = dd[0][0][1][0] - dd[0][0][1][1] - dd[1][0][0][0] + dd[1][0][0][1];
+      cf[2 * cplane + co + cside + 1] =
+          Zl + dd[0][0][1][1] - dd[0][1][1][0] - dd[1][0][0][1] + dd[1][1][0][0];
+    }
+    __syncthreads();
+  };
+  for (int l = 0; l + 2 < m; ++l) ancestor_level(l);  // uses group A only
+  cp_async_wait_all();
+  __syncthreads();
+  if (m >= 2) ancestor_level(m - 2);                  // level m-1 fields (group B)
+
+  // ---- (1') level m-1 -> m, all three fields per parent, parity-split child planes
+  {
+    const int l = m - 1;
+    const int ys = sR[0][0][l], xs = sR[1][0][l];
+    constexpr int DW = G::P1 + 1, DPL = DW * DW;
+    const float* dt = sDet + sDoff[l];
+    const FT asc = FT(pow2f(l));
+    int poy = 0, pox = 0;
+    if (l > 0) {
+      poy = ys - 2 * sR[0][0][l - 1];
+      pox = xs - 2 * sR[1][0][l - 1];
+    }
+    constexpr int NP = G::P1 * G::P1;
+#pragma unroll 1
+    for (int idx = tid; idx < NP; idx += kThreads) {
+      const int pi = idx / G::P1, pj = idx - pi * G::P1;  // constant divisor
+      const int o = pi * DW + pj;
+      FT H[4], V[4], D[4];  // cells (i,j), (i,j+1), (i+1,j), (i+1,j+1)
+      const int oo[4] = {o, o + 1, o + DW, o + DW + 1};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        H[q] = FT(dt[oo[q]]) * asc;
+        V[q] = FT(dt[DPL + oo[q]]) * asc;
+        D[q] = FT(dt[2 * DPL + oo[q]]) * asc;
+      }
+      const FT d00 = H[0] + V[0] + D[0], d01 = -H[0] + V[0] - D[0], d10 = H[0] - V[0] - D[0],
+               d11 = -H[0] - V[0] + D[0];
+      const FT r00 = H[1] + V[1] + D[1], r10 = H[1] - V[1] - D[1];
+      const FT b00 = H[2] + V[2] + D[2], b01 = -H[2] + V[2] - D[2];
+      const FT g00 = H[3] + V[3] + D[3];
+      FT Xl = FT(0), Yl = FT(0), Zl = FT(0);
+      if (l > 0) {
+        const int po = (pi + poy) * CB + (pj + pox);
+        Xl = sB1[po];
+        Yl = sB1[CB * CB + po];
+        Zl = sB1[2 * CB * CB + po];
+      }
+      FT* c0 = sCh + (2 * pi) * HC + pj;  // field 0, even plane, row 2pi
+      // X
+      c0[0] = d00 - d01;
+      c0[PLANE_C] = Xl + d01 - r00;
+      c0[HC] = d10 - d11;
+      c0[PLANE_C + HC] = Xl + d11 - r10;
+      // Y
+      FT* c1 = c0 + 2 * PLANE_C;
+      c1[0] = d00 - d10;
+      c1[PLANE_C] = d01 - d11;
+      c1[HC] = Yl + d10 - b00;
+      c1[PLANE_C + HC] = Yl + d11 - b01;
+      // Z
+      FT* c2 = c0 + 4 * PLANE_C;
+      c2[0] = FT(4) * D[0];
+      c2[PLANE_C] = d01 - d11 - r00 + r10;
+      c2[HC] = d10 - d11 - b00 + b01;
+      c2[PLANE_C + HC] = Zl + d11 - r10 - b01 + g00;
     }
     __syncthreads();
   }
 
-  // ---- level m-1 -> m per field, fused with (2) shift and the first bottom-up step.
-  //      The level-m children are stored column-parity split (sBig[c & 1][r][c >> 1]) so that the
-  //      stencil's lanes read consecutive words; the shifted level-(m-1) field fld overwrites
-  //      plane fld of sFB once its children are built.
-  const int Sn1 = ((tc + 1) << (k - 1)) - 1;
+  // ---- (2)+(3) fused shift + first bottom-up: register-sliding window down each thread's strip,
+  //      taps at immediate offsets; shifted level-(m-1) fields -> sB1, owned outputs -> global
   {
-    const int l = m - 1;
-    const int ys = sR[0][0][l], yn = sR[0][1][l], xs = sR[1][0][l], xn = sR[1][1][l];
-    const int dn = xn + 1, dplane = (yn + 1) * dn;
-    const float* dt = sDet + sDoff[l];
-    const FT asc = FT(pow2f(l));
-    int pstride = 0, poy = 0, pox = 0;
-    if (l > 0) {
-      pstride = 2 * sR[1][1][l - 1];
-      poy = ys - 2 * sR[0][0][l - 1];
-      pox = xs - 2 * sR[1][0][l - 1];
-    }
-    const int hs = xn;                   // half-row stride of the parity-split children
-    const int hplane = 2 * yn * xn;      // one parity plane
-    const int Cy = 2 * ys;               // unwrapped origin (rows) of the level-m window
-    const int Ssy = i0 << (k - 1), Ssx = j0 << (k - 1);
-    const int On = tc << (k - 1);
+    const int k1 = K - 1;
+    const int Ssy = i0 << k1, Ssx = j0 << k1;
+    constexpr int ON1 = TC << (K - 1);
+    const int Cy = 2 * sR[0][0][m - 1], Cx = 2 * sR[1][0][m - 1];
     const FT wy1 = FT(P.wy), wx1 = FT(P.wx);
     const FT wy0 = FT(1) - wy1, wx0 = FT(1) - wx1;
-    // fused tap weights: [1,1]*[w0,w1] = [w1, 1, w0]; [1,2,1]*[w0,w1] = [w1, w0+2w1, 2w0+w1, w0]
-    const FT B3y[3] = {wy1, FT(1), wy0}, B3x[3] = {wx1, FT(1), wx0};
-    const FT T4y[4] = {wy1, wy0 + FT(2) * wy1, FT(2) * wy0 + wy1, wy0};
-    const FT T4x[4] = {wx1, wx0 + FT(2) * wx1, FT(2) * wx0 + wx1, wx0};
-    // column tap v in -1..2 lands in parity plane (v - Qx) & 1, half-column offset floor((v - Qx) / 2)
-    int tapo[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) tapo[v] = ((v - 1 - P.Qx) & 1) * hplane + ((v - 1 - P.Qx) >> 1);
+    const FT ta = wx1, tb0 = wx0 + FT(2) * wx1, tb1 = FT(2) * wx0 + wx1, tcc = wx0;
+    const FT ua = wy1, ub0 = wy0 + FT(2) * wy1, ub1 = FT(2) * wy0 + wy1, uc = wy0;
     const FT q = FT(0.25);
     const int lv = m - 1;
     const int gl = 1 << lv;
     const FT osc = FT(pow2f(-lv));
     const bool emit = lv < band;
-    for (int fld = 0; fld < 3; ++fld) {
-      const FT* pfp = sFB + fld * CB * CB;
-      for (Walk2 w(yn * xn, xn); w.idx < yn * xn; w.next()) {
-        const int pi = w.r, pj = w.c;
-        const int o00 = pi * dn + pj;
-        FT Fl = FT(0);
-        if (l > 0) Fl = pfp[(pi + poy) * pstride + (pj + pox)];
-        FT* ce = sBig + (2 * pi) * hs + pj;  // even child column 2pj
-        FT* co = ce + hplane;                // odd child column 2pj+1
-        const FT H = FT(dt[o00]) * asc, V = FT(dt[dplane + o00]) * asc, D = FT(dt[2 * dplane + o00]) * asc;
-        const FT d00 = H + V + D, d01 = -H + V - D, d10 = H - V - D, d11 = -H - V + D;
-        if (fld == 0) {
-          const int o = o00 + 1;
-          const FT Hr = FT(dt[o]) * asc, Vr = FT(dt[dplane + o]) * asc, Dr = FT(dt[2 * dplane + o]) * asc;
-          const FT r00 = Hr + Vr + Dr, r10 = Hr - Vr - Dr;
-          ce[0] = d00 - d01;
-          co[0] = Fl + d01 - r00;
-          ce[hs] = d10 - d11;
-          co[hs] = Fl + d11 - r10;
-        } else if (fld == 1) {
-          const int o = o00 + dn;
-          const FT Hb = FT(dt[o]) * asc, Vb = FT(dt[dplane + o]) * asc, Db = FT(dt[2 * dplane + o]) * asc;
-          const FT b00 = Hb + Vb + Db, b01 = -Hb + Vb - Db;
-          ce[0] = d00 - d10;
-          co[0] = d01 - d11;
-          ce[hs] = Fl + d10 - b00;
-          co[hs] = Fl + d11 - b01;
-        } else {
-          const int o01 = o00 + 1, o10 = o00 + dn, o11 = o00 + dn + 1;
-          const FT Hr = FT(dt[o01]) * asc, Vr = FT(dt[dplane + o01]) * asc, Dr = FT(dt[2 * dplane + o01]) * asc;
-          const FT Hb = FT(dt[o10]) * asc, Vb = FT(dt[dplane + o10]) * asc, Db = FT(dt[2 * dplane + o10]) * asc;
-          const FT Hd = FT(dt[o11]) * asc, Vd = FT(dt[dplane + o11]) * asc, Dd = FT(dt[2 * dplane + o11]) * asc;
-          const FT r00 = Hr + Vr + Dr, r10 = Hr - Vr - Dr;
-          const FT b00 = Hb + Vb + Db, b01 = -Hb + Vb - Db;
-          const FT g00 = Hd + Vd + Dd;
-          ce[0] = FT(4) * D;
-          co[0] = d01 - d11 - r00 + r10;
-          ce[hs] = d10 - d11 - b00 + b01;
-          co[hs] = Fl + d11 - r10 - b01 + g00;
+    const int strip = tid / SN1, jj = tid - strip * SN1;
+    if (strip < G::NSTRIP) {
+      const int ii0 = strip * G::RSS;
+      const int rb = 2 * (Ssy + ii0) - P.Qy - Cy - 1;  // window row 0 = tap -1 of row ii0
+      constexpr int NW = 2 * G::RSS + 2;
+#pragma unroll
+      for (int fld = 0; fld < 3; ++fld) {
+        const FT* pl = sCh + fld * 2 * PLANE_C;
+        const FT* base[4];
+#pragma unroll
+        for (int vv = 0; vv < 4; ++vv) {
+          const int cl = 2 * (Ssx + jj) - P.Qx - Cx + vv - 1;
+          base[vv] = pl + (cl & 1) * PLANE_C + rb * HC + (cl >> 1);
         }
-      }
-      __syncthreads();
-      FT* dstS = sFB + fld * CB * CB;  // level m-1 field fld is dead now
-      float* ob = out + (long long)gl * gl * (1 + fld);
-      for (Walk2 w(Sn1 * Sn1, Sn1); w.idx < Sn1 * Sn1; w.next()) {
-        const int ii = w.r, jj = w.c;
-        const int gi = Ssy + ii, gj = Ssx + jj;
-        const FT* base = sBig + (2 * gi - P.Qy - Cy) * hs + (gj - xs);
-        FT acc = FT(0), det = FT(0);
-        if (fld == 0) {  // X: rows [w1,1,w0] (u=-1..1), cols tent (v=-1..2)
+        FT hA[NW], hB[NW];
 #pragma unroll
-          for (int u = -1; u <= 1; ++u) {
-            const FT* rp = base + u * hs;
-            const FT x_1 = rp[tapo[0]], x0 = rp[tapo[1]], x1 = rp[tapo[2]], x2 = rp[tapo[3]];
-            acc += B3y[u + 1] * (T4x[0] * x_1 + T4x[1] * x0 + T4x[2] * x1 + T4x[3] * x2);
-            det += B3y[u + 1] * (wx1 * x_1 + wx0 * x0);
-          }
-        } else if (fld == 1) {  // Y: rows tent (u=-1..2), cols [w1,1,w0] (v=-1..1)
-#pragma unroll
-          for (int u = -1; u <= 2; ++u) {
-            const FT* rp = base + u * hs;
-            const FT r = B3x[0] * rp[tapo[0]] + B3x[1] * rp[tapo[1]] + B3x[2] * rp[tapo[2]];
-            acc += T4y[u + 1] * r;
-            if (u == -1) det += wy1 * r;
-            if (u == 0) det += wy0 * r;
-          }
-        } else {  // Z: tent x tent
-#pragma unroll
-          for (int u = -1; u <= 2; ++u) {
-            const FT* rp = base + u * hs;
-            const FT z_1 = rp[tapo[0]], z0 = rp[tapo[1]], z1 = rp[tapo[2]], z2 = rp[tapo[3]];
-            acc += T4y[u + 1] * (T4x[0] * z_1 + T4x[1] * z0 + T4x[2] * z1 + T4x[3] * z2);
-            const FT dr = wx1 * z_1 + wx0 * z0;
-            if (u == -1) det += wy1 * dr;
-            if (u == 0) det += wy0 * dr;
+        for (int w = 0; w < NW; ++w) {
+          const FT x_1 = base[0][w * HC], x0 = base[1][w * HC], x1 = base[2][w * HC];
+          if (fld == 1) {
+            hA[w] = wx1 * x_1 + x0 + wx0 * x1;
+            hB[w] = hA[w];
+          } else {
+            const FT x2 = base[3][w * HC];
+            hA[w] = ta * x_1 + tb0 * x0 + tb1 * x1 + tcc * x2;
+            hB[w] = wx1 * x_1 + wx0 * x0;
           }
         }
-        dstS[ii * Sn1 + jj] = q * acc;
-        if (ii < On && jj < On && emit)
-          ob[gi * gl + gj] = (float)(q * det * osc);
+        FT* dstS = sB1 + fld * CB * CB;
+        float* ob = out + (long long)gl * gl * (1 + fld);
+#pragma unroll
+        for (int r = 0; r < G::RSS; ++r) {
+          const int ii = ii0 + r;
+          if (ii < SN1) {
+            const int u = 2 * r;
+            FT fv, dv;
+            if (fld == 0) {
+              fv = q * (wy1 * hA[u] + hA[u + 1] + wy0 * hA[u + 2]);
+              dv = q * (wy1 * hB[u] + hB[u + 1] + wy0 * hB[u + 2]);
+            } else {
+              fv = q * (ua * hA[u] + ub0 * hA[u + 1] + ub1 * hA[u + 2] + uc * hA[u + 3]);
+              dv = q * (wy1 * hB[u] + wy0 * hB[u + 1]);
+            }
+            dstS[ii * SN1 + jj] = fv;
+            if (ii < ON1 && jj < ON1 && emit) ob[(Ssy + ii) * gl + (Ssx + jj)] = (float)(dv * osc);
+          }
+        }
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
 
-  // ---- (3) plain bottom-up for levels m-2 .. c on the shifted windows (sFB <-> sFS)
-  const FT* srcS = sFB;
-  int srcN = Sn1, srcPlane = CB * CB;
-  for (int lev = m - 2; lev >= c; --lev) {
-    const int e = lev - c;
-    const int Sn = ((tc + 1) << e) - 1;
-    const int On = tc << e;
+  // ---- (3) plain bottom-up for levels m-2 .. c (compile-time windows), sB1 <-> sCh
+  const FT* srcS = sB1;
+  int srcN = SN1, srcPlane = CB * CB;
+  const FT q = FT(0.25);
+#pragma unroll
+  for (int e = K - 2; e >= 0; --e) {
+    const int lev = c + e;
+    const int Sn = G::SN(e);
+    const int On = TC << e;
     const int Ssy = i0 << e, Ssx = j0 << e;
-    const bool to_small = ((m - 2 - lev) & 1) == 0;
-    FT* dst = to_small ? sFS : sFB;
-    const int dstPlane = to_small ? CSM * CSM : CB * CB;
+    FT* dst = ((K - 2 - e) & 1) == 0 ? sCh : sB1;
+    const int dstPlane = ((K - 2 - e) & 1) == 0 ? Sn * Sn : CB * CB;
     const int gl = 1 << lev;
     const FT osc = FT(pow2f(-lev));
-    const FT q = FT(0.25);
     const bool emit = lev < band;
-    for (Walk2 w(Sn * Sn, Sn); w.idx < Sn * Sn; w.next()) {
-      const int ii = w.r, jj = w.c;
+    const float inv_sn = inv_small(Sn);
+    for (int idx = tid; idx < Sn * Sn; idx += kThreads) {
+      const int ii = div_small(idx, inv_sn), jj = idx - ii * Sn;
       const int a2 = 2 * ii, b2 = 2 * jj;
       const FT* X = srcS + a2 * srcN + b2;
       const FT* Y = srcS + srcPlane + a2 * srcN + b2;
@@ -439,15 +489,14 @@ __global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_con
       const FT Yn = q * (Y[0] + FT(2) * Y[srcN] + Y[2 * srcN] + Y[1] + FT(2) * Y[srcN + 1] + Y[2 * srcN + 1]);
       const FT Zn = q * ((Z[0] + FT(2) * Z[1] + Z[2]) + FT(2) * (Z[srcN] + FT(2) * Z[srcN + 1] + Z[srcN + 2]) +
                          (Z[2 * srcN] + FT(2) * Z[2 * srcN + 1] + Z[2 * srcN + 2]));
-      const FT hx = q * (X[0] + X[srcN]), vy = q * (Y[0] + Y[1]), dz = q * Z[0];
       dst[ii * Sn + jj] = Xn;
       dst[dstPlane + ii * Sn + jj] = Yn;
       dst[2 * dstPlane + ii * Sn + jj] = Zn;
       if (ii < On && jj < On && emit) {
-        const long long o = (long long)(Ssy + ii) * gl + (Ssx + jj);
-        out[(long long)gl * gl * 1 + o] = (float)(hx * osc);
-        out[(long long)gl * gl * 2 + o] = (float)(vy * osc);
-        out[(long long)gl * gl * 3 + o] = (float)(dz * osc);
+        const int o = (Ssy + ii) * gl + (Ssx + jj);
+        out[(long long)gl * gl * 1 + o] = (float)(q * (X[0] + X[srcN]) * osc);
+        out[(long long)gl * gl * 2 + o] = (float)(q * (Y[0] + Y[1]) * osc);
+        out[(long long)gl * gl * 3 + o] = (float)(q * Z[0] * osc);
       }
     }
     __syncthreads();
@@ -455,7 +504,7 @@ __global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_con
     srcN = Sn;
     srcPlane = dstPlane;
   }
-  // srcS now holds the shifted level-c fields over the owned tile (srcN = tc)
+  // srcS holds the shifted level-c fields over the owned tile (srcN = TC when K >= 2; SN1 = TC when K = 1)
 
   if (blockIdx.x == 0 && tid == 0) out[0] = __ldg(in);  // scaling coefficient: unchanged (R8)
   if (c == 0) return;
@@ -463,19 +512,19 @@ __global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_con
   // ---- publish the owned level-c fields; the last tile of the face runs the coarse finish
   const int gc = 1 << c;
   FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
-  for (int idx = tid; idx < 3 * tc * tc; idx += kThreads) {
-    const int fld = idx / (tc * tc), r = idx - fld * tc * tc;
-    const int ii = r / tc, jj = r - ii * tc;
+  for (int idx = tid; idx < 3 * TC * TC; idx += kThreads) {
+    const int fld = idx / (TC * TC), r = idx - fld * TC * TC;
+    const int ii = r / TC, jj = r - ii * TC;
     wsf[(long long)fld * gc * gc + (long long)(i0 + ii) * gc + (j0 + jj)] = srcS[fld * srcPlane + ii * srcN + jj];
   }
   __threadfence();
   __syncthreads();
   if (tid == 0) {
     const unsigned prev = atomicAdd(args.counters + g, 1u);
-    sLast = (prev == (unsigned)(tpr * tpr - 1));
+    *sLast = (prev == (unsigned)(tpr * tpr - 1));
   }
   __syncthreads();
-  if (!sLast) return;
+  if (!*sLast) return;
   __threadfence();
   const long long need = 3ll * gc * gc + 3ll * (gc / 2) * (gc / 2);
   if (need * (long long)sizeof(FT) <= (long long)S::BYTES) {
@@ -486,6 +535,43 @@ __global__ void __launch_bounds__(kThreads) shift2d_tile_kernel(const __grid_con
     coarse_finish<FT>(A, B0, A, c, out, band, false);
   } else {
     coarse_finish<FT>(wsf, wsf + 3ll * gc * gc, wsf, c, out, band, true);
+  }
+}
+
+template <typename FT>
+constexpr int max_tile_smem() {
+  int a = TSmem<FT, 3, 8>::BYTES, b = TSmem<FT, 3, 4>::BYTES;
+  return a > b ? a : b;
+}
+
+template <typename FT>
+__global__ void __launch_bounds__(kThreads, 2) shift2d_tile_kernel(const __grid_constant__ ShiftArgs args) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int sR[2][2][HS_MAX_LOG2N + 1];
+  __shared__ int sDoff[HS_MAX_LOG2N + 2];
+  __shared__ int sLast;
+  const int g = blockIdx.y;  // face within this launch
+  const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
+  const int m = P.m;
+  if (m == 0) return;  // identity: handled by permute_kernel
+  const int c = m > KF ? m - KF : 0;
+  const int k = m - c;
+  const int tc = (1 << c) < TC ? (1 << c) : TC;
+  const int tpr = (1 << c) / tc;
+  if ((int)blockIdx.x >= tpr * tpr) return;
+  const int i0 = (blockIdx.x / tpr) * tc;
+  const int j0 = (blockIdx.x % tpr) * tc;
+  if (k == 3) {
+    switch (tc) {
+      case 8: tile_body<FT, 3, 8>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
+      case 4: tile_body<FT, 3, 4>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
+      case 2: tile_body<FT, 3, 2>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
+      default: tile_body<FT, 3, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
+    }
+  } else if (k == 2) {
+    tile_body<FT, 2, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast);
+  } else {
+    tile_body<FT, 1, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast);
   }
 }
 
@@ -527,11 +613,11 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, cudaStream_t st) {
   static bool attr_done = false;  // idempotent attribute set (benign race: same value)
   if (!attr_done) {
     HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_tile_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Smem<FT>::BYTES),
+                                       max_tile_smem<FT>()),
                   "cudaFuncSetAttribute(shift2d_tile_kernel)");
     attr_done = true;
   }
-  shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, Smem<FT>::BYTES, st>>>(a);
+  shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);
   HS_CHECK_LAUNCH("shift2d_tile_kernel");
   return HS_OK;
 }
