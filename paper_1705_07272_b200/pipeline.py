@@ -1,0 +1,84 @@
+"""Host-buffer serving pipeline for the hot path: one call per step takes the frames' light
+pyramids and shifts in pinned HOST memory and returns radiance in pinned HOST memory.
+
+Plumbing only (torch streams, events and async copies); both compute steps are the C-ABI kernels
+(``haar_shift_coeffs``, ``relight_vertices``).  Overlap, per step i:
+
+    h2d stream   : light_i  -> device buffer (i % 2)            (waits until step i-2's shift read it)
+    compute      : shift(light_i) ; relight chunk 0 ; relight chunk 1 ; ...
+    d2h stream   :                  R chunk 0 -> host ; R chunk 1 -> host ; ...
+
+so the H2D of step i+1 runs under step i's relight, and every radiance chunk is copied back while
+the next chunk computes; H2D and D2H use different copy engines (full duplex).  Every step still
+moves its own inputs in and its own result out.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import api
+from .dist import chunk_bounds
+
+
+class ShiftRelightPipeline:
+    def __init__(self, transfer: torch.Tensor, faces: int, log2n: int, batch: int, band_levels: int,
+                 chunks: int = 8, full_pyramids: bool = True):
+        dev = transfer.device
+        N = 1 << log2n
+        self.T = transfer
+        self.faces, self.log2n, self.batch = faces, log2n, batch
+        self.band = band_levels
+        self.k_face = 4 ** band_levels
+        self.full = full_pyramids
+        self.V = transfer.shape[0]
+        self.light = [torch.empty((batch, faces, N * N), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.shifted = torch.empty((batch, faces, N * N if full_pyramids else self.k_face), dtype=torch.float32,
+                                   device=dev)
+        self.R = torch.empty((self.V, batch), dtype=torch.float32, device=dev)
+        ws = api.haar_shift_workspace_bytes(2, log2n, faces, batch)
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+        rws = api.relight_workspace_bytes(faces, self.k_face, batch)
+        self.rws = None
+        if rws:
+            raw = torch.empty(rws + 1024, dtype=torch.uint8, device=dev)
+            self.rws = raw[(-raw.data_ptr()) % 1024:]
+        self.chunks = chunk_bounds(self.V, chunks)
+        self.compute = torch.cuda.current_stream(dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        self.ev_light_free = [torch.cuda.Event() for _ in range(2)]
+        self.ev_chunk = [torch.cuda.Event() for _ in self.chunks]
+        self.ev_copied = [torch.cuda.Event() for _ in self.chunks]
+        self.i = 0
+        self.launches = 0
+
+    def step(self, light_host: torch.Tensor, shifts, radiance_host: torch.Tensor) -> torch.cuda.Event:
+        """Enqueue one step; returns an event that completes when radiance_host holds the result."""
+        buf = self.i & 1
+        with torch.cuda.stream(self.h2d):
+            if self.i >= 2:
+                self.h2d.wait_event(self.ev_light_free[buf])
+            self.light[buf].copy_(light_host, non_blocking=True)
+            self.ev_h2d[buf].record(self.h2d)
+        self.compute.wait_event(self.ev_h2d[buf])
+        api.haar_shift_coeffs(self.light[buf], shifts, 2, self.log2n if self.full else self.band, out=self.shifted,
+                              workspace=self.ws, stream=self.compute)
+        self.launches += api.last_launch_count()
+        self.ev_light_free[buf].record(self.compute)
+        for c, (s, n) in enumerate(self.chunks):
+            if self.i >= 1:
+                self.compute.wait_event(self.ev_copied[c])  # previous step's D2H of this chunk is done
+            api.relight_vertices(self.T[s:s + n], self.shifted, self.faces, self.k_face, out=self.R[s:s + n],
+                                 workspace=self.rws, stream=self.compute)
+            self.launches += api.last_launch_count()
+            self.ev_chunk[c].record(self.compute)
+            self.d2h.wait_event(self.ev_chunk[c])
+            with torch.cuda.stream(self.d2h):
+                radiance_host[s:s + n].copy_(self.R[s:s + n], non_blocking=True)
+                self.ev_copied[c].record(self.d2h)
+        self.i += 1
+        return self.ev_copied[-1]

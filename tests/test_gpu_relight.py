@@ -109,3 +109,28 @@ def test_relight_shifted_c4_subset():
     torch.cuda.synchronize()
     ref = orelight.relight_shifted(T.cpu().numpy(), L, sv.astype(np.float64))
     assert _rel(R.cpu().numpy(), ref) <= TOL
+
+
+def test_host_pipeline_matches_device_calls():
+    """ShiftRelightPipeline (host buffers, overlapped copies) returns exactly the device path's
+    radiance, step after step (double-buffered light, chunked D2H)."""
+    import torch
+    import paper_1705_07272_b200 as hs
+    from paper_1705_07272_b200.pipeline import ShiftRelightPipeline
+    n, F, B, V, band = 5, 6, 64, 1000, 3
+    T = torch.empty((V, F * 4 ** band), dtype=torch.float32, device="cuda")
+    hs.hs_fill_transfer(T, 0, F, 4 ** band, 31, synth.STREAM_T)
+    pipe = ShiftRelightPipeline(T, F, n, B, band, chunks=3)
+    outs, refs = [], []
+    for step in range(3):
+        light = synth.light_pyramids(40 + step, B, F, n)
+        sh = np.random.default_rng(step).uniform(0, 32, size=(B, F, 2))
+        lh = torch.from_numpy(light).pin_memory()
+        rh = torch.empty((V, B), dtype=torch.float32).pin_memory()
+        pipe.step(lh, sh, rh)
+        outs.append(rh)
+        s = hs.haar_shift_coeffs(torch.from_numpy(light).cuda(), sh, 2)
+        refs.append(hs.relight_vertices(T, s, F, 4 ** band).cpu())
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
