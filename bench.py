@@ -390,7 +390,7 @@ def run_ours(args, cfg):
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:
-            full, desc = oracle_sample(cfg, 1, 4000)
+            full, desc = oracle_sample(cfg, 16, 400000)
             line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                                     "sample": desc}
         print(json.dumps(line), flush=True)

@@ -38,32 +38,27 @@
 
 #include "common.cuh"
 
+#ifdef HS_PHASE_TIMING  // debug builds only: per-CTA clock64 at phase boundaries
+__device__ long long g_phase[1 << 18];
+#define HS_PHASE(k)                                                                                   \
+  if (threadIdx.x == 0 && ((long long)blockIdx.y * gridDim.x + blockIdx.x) < (1 << 14))             \
+    hs::g_phase_ptr()[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = clock64();
+namespace hs {
+__device__ __forceinline__ long long* g_phase_ptr() { return g_phase; }
+}
+extern "C" HS_API int hs_debug_phase_dump(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_phase, (size_t)n * sizeof(long long));
+}
+#else
+#define HS_PHASE(k)
+#endif
+
 namespace hs {
 namespace {
 
 constexpr int KF = kTileKF;
 constexpr int TC = kTileTC;
 constexpr int kThreads = 256;
-// compile-time maxima of the per-axis region sizes
-constexpr int PM1 = (1 << (KF - 1)) * (TC + 1) + 1;   // parents at level m-1          (37)
-constexpr int PM2 = (1 << (KF - 2)) * (TC + 1) + 1;   // parents at level m-2          (19)
-constexpr int CB = 2 * PM2;                            // level m-1 field plane side    (38)
-constexpr int CSM = PM2 + 1;                           // level <= m-2 field plane side (20)
-constexpr int CM = 2 * PM1;                            // level m children plane side   (74)
-constexpr int SM1 = (1 << (KF - 1)) * (TC + 1) - 1;   // shifted window at m-1         (35)
-constexpr int SM2 = (1 << (KF - 2)) * (TC + 1) - 1;   // shifted window at m-2         (17)
-constexpr int DET_FLOATS = 6336;                       // all detail windows, <= 12 levels
-static_assert(SM1 <= CB && SM2 <= CSM && PM1 <= CB, "aliasing assumptions");
-
-template <typename FT>
-struct Smem {
-  static constexpr int DET = 0;                                        // float[DET_FLOATS]
-  static constexpr int FB = DET + DET_FLOATS * 4;                       // FT[3][CB*CB]
-  static constexpr int FS = FB + 3 * CB * CB * (int)sizeof(FT);         // FT[3][CSM*CSM]
-  static constexpr int BIG = FS + 3 * CSM * CSM * (int)sizeof(FT);      // FT[CM*CM]
-  static constexpr int BYTES = BIG + CM * CM * (int)sizeof(FT);
-};
-
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                "l"(src)
@@ -80,30 +75,6 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // least 1/(2n) away from an integer and the float error is < 2^-21 * 2^16 / n, so the floor is exact.
 __device__ __forceinline__ int div_small(int x, float inv_n) { return __float2int_rd(((float)x + 0.5f) * inv_n); }
 __device__ __forceinline__ float inv_small(int n) { return __fdividef(1.0f, (float)n); }
-
-// Block-stride walk over a rows x cols grid (flat index idx = r * cols + c) without an integer
-// division: one reciprocal division at the start, then incremental row/column updates.
-struct Walk2 {
-  int idx, r, c, dr, dc, cols;
-  __device__ __forceinline__ Walk2(int total, int ncols) : cols(ncols) {
-    const float inv = inv_small(ncols);
-    idx = threadIdx.x;
-    r = div_small(idx, inv);
-    c = idx - r * cols;
-    dr = div_small(blockDim.x, inv);
-    dc = blockDim.x - dr * cols;
-    (void)total;
-  }
-  __device__ __forceinline__ void next() {
-    idx += blockDim.x;
-    r += dr;
-    c += dc;
-    if (c >= cols) {
-      c -= cols;
-      ++r;
-    }
-  }
-};
 
 // Coarse bottom-up of one face from the shifted level-c fields (periodic full grid) to level 0.
 // src/dst may point to shared or global memory (generic addressing); global reads use ld.cg.
@@ -169,11 +140,12 @@ struct TGeo {
   static constexpr int SN1 = SN(K - 1);
   static constexpr int NSTRIP = (kThreads / SN1 < SN1) ? kThreads / SN1 : SN1;
   static constexpr int RSS = (SN1 + NSTRIP - 1) / NSTRIP;      // fused-stencil rows per strip
-  static constexpr int CHR = CH + 2 * (NSTRIP * RSS - SN1) + 4; // child plane rows incl. spare
+  static constexpr int CHR = CH + 2 * (NSTRIP * RSS - SN1);     // child plane rows incl. spare
   static constexpr int DETW(int d) { return P(d) + 1; }
+  static constexpr int WS1 = (DETW(1) + 6 + 3) / 4 * 4;  // padded row of the level m-1 window (16B chunks)
   static constexpr int DET_MAX = [] {
-    int o = 0;
-    for (int d = 1; d <= HS_MAX_LOG2N; ++d) o += 3 * DETW(d) * DETW(d);
+    int o = 3 * DETW(1) * WS1;
+    for (int d = 2; d <= HS_MAX_LOG2N; ++d) o += 3 * DETW(d) * DETW(d);
     return o;
   }();
   static constexpr int ANC_MAX = 2 * P(3) > 2 * P(4) ? 2 * P(3) : 2 * P(4);  // level <= m-2 side
@@ -190,13 +162,62 @@ struct TSmem {
   static_assert(3 * G::SN1 * G::SN1 <= 3 * G::CB * G::CB, "shifted m-1 window aliases B1");
 };
 
+// Detail windows of levels l = m - d for d in [D, DEND] (d <= m): [3][W][W] floats each with the
+// compile-time side W = P(d) + 1, gathered element-wise (periodic) with cp.async.
+template <class G, int D, int DEND>
+__device__ __forceinline__ void load_windows(const float* __restrict__ in, float* sDet,
+                                             const int (*sR)[2][HS_MAX_LOG2N + 1], const int* sDoff, int m) {
+  if constexpr (D <= DEND) {
+    if (D <= m) {
+      constexpr int W = G::DETW(D), PER = W * W;
+      const int l = m - D;
+      const int ys = sR[0][0][l], xs = sR[1][0][l], mask = (1 << l) - 1;
+      float* dst = sDet + sDoff[l];
+      for (int e = threadIdx.x; e < 3 * PER; e += kThreads) {
+        const int t = e / PER, rem = e - t * PER;
+        const int a = rem / W, bb = rem - a * W;
+        cp_async4(dst + e, in + (((1 + t) << (2 * l)) + (((ys + a) & mask) << l) + ((xs + bb) & mask)));
+      }
+      load_windows<G, D + 1, DEND>(in, sDet, sR, sDoff, m);
+    }
+  }
+}
+
+// Level m-1 window (d = 1) with 16-byte cp.async: every row covers the same (periodic) column
+// range [xs, xs + W); it is stored with row stride WS1 at smem column (col - xs) + (xs & 3), so the
+// aligned global chunks of both segments of a wrapping row land 16-byte aligned in smem.
+template <class G>
+__device__ __forceinline__ void load_window_vec(const float* __restrict__ in, float* sDet,
+                                                const int (*sR)[2][HS_MAX_LOG2N + 1], const int* sDoff, int m) {
+  constexpr int W = G::DETW(1), WS = G::WS1, NCH = WS / 4, ROWS = 3 * W;
+  const int l = m - 1;
+  const int gl = 1 << l, mask = gl - 1;
+  const int ys = sR[0][0][l];
+  const int xsm = sR[1][0][l] & mask;
+  const int c0 = xsm & ~3;
+  const bool wrap = xsm + W > gl;
+  const int n1 = ((wrap ? gl : ((xsm + W + 3) & ~3)) - c0) >> 2;     // chunks of segment 1
+  const int ntot = n1 + (wrap ? ((xsm + W - gl + 3) >> 2) : 0);
+  float* dst = sDet + sDoff[l];
+  for (int e = threadIdx.x; e < ROWS * NCH; e += kThreads) {
+    const int row = e / NCH, k = e - row * NCH;
+    if (k >= ntot) continue;
+    const int t = row / W, a = row - t * W;
+    const int col = (k < n1) ? c0 + 4 * k : 4 * (k - n1);
+    const float* src = in + ((1 + t) << (2 * l)) + (((ys + a) & mask) << l) + col;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst + row * WS + 4 * k)),
+                 "l"(src)
+                 : "memory");
+  }
+}
+
 template <typename FT, int K, int TC>
 __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* smem, const FaceParam& P, int g,
                                           int m, int c, int i0, int j0, int tpr, int (*sR)[2][HS_MAX_LOG2N + 1],
                                           int* sDoff, int* sLast) {
   using G = TGeo<K, TC>;
   using S = TSmem<FT, K, TC>;
-  constexpr int CB = G::CB, CH = G::CH, HC = G::HC, CHR = G::CHR, SN1 = G::SN1;
+  constexpr int CB = G::CB, HC = G::HC, CHR = G::CHR, SN1 = G::SN1;
   constexpr int PLANE_C = CHR * HC;  // one parity plane of one field's children
   const int n = args.log2n;
   const int b = g / args.faces, f = g % args.faces;
@@ -209,6 +230,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   FT* sB1 = reinterpret_cast<FT*>(smem + S::B1);
   FT* sCh = reinterpret_cast<FT*>(smem + S::CHILD);
 
+  HS_PHASE(0)
   // ---- window starts: level-m window [2^K i0 - Q - 1, + FW); level m-d starts at floor(s/2^d)
   if (tid < 2) {
     const int Q = tid == 0 ? P.Qy : P.Qx;
@@ -219,60 +241,38 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
       sR[tid][0][l] = s;
     }
   }
-  if (tid == 0) {  // detail window of level l = m-d has side P(d)+1 (compile-time table)
-    int off = 0;
+  if (tid == 0) {  // window side of level l = m-d: P(d) = P(d-1)/2 + 1, P(0) = FW (O(m), incremental)
+    int off = 0, p = G::FW;
     for (int l = m - 1; l >= 0; --l) {
+      p = p / 2 + 1;
       sDoff[l] = off;
-      const int w = G::DETW(m - l);
-      off += 3 * w * w;
-      sR[0][1][l] = G::P(m - l);
-      sR[1][1][l] = G::P(m - l);
+      off += (l == m - 1) ? 3 * (p + 1) * G::WS1 : 3 * (p + 1) * (p + 1);
+      sR[0][1][l] = p;
+      sR[1][1][l] = p;
     }
     sDoff[m] = off;
   }
   __syncthreads();
 
-  // ---- detail windows in two cp.async groups (flat loops, level pointer monotone per thread):
-  //      group A = ancestors' windows (levels <= m-3), group B = the large windows of levels
-  //      m-2 and m-1; the ancestors' top-down runs while group B is still in flight.
-  {
-    auto load_range = [&](int lhi, int llo) {  // levels lhi down to llo (stored m-1 first)
-      if (lhi < llo) return;
-      const int beg = sDoff[lhi], total = sDoff[llo] + 3 * (sR[0][1][llo] + 1) * (sR[0][1][llo] + 1);
-      int l = lhi + 1, lbeg = 0, lend = beg, w = 1, per = 1, ys = 0, xs = 0, mask = 0;
-      float inv_per = 1.f, inv_w = 1.f;
-      for (int e = beg + tid; e < total; e += kThreads) {
-        while (e >= lend) {
-          --l;
-          lbeg = sDoff[l];
-          w = sR[0][1][l] + 1;
-          per = w * w;
-          lend = lbeg + 3 * per;
-          ys = sR[0][0][l];
-          xs = sR[1][0][l];
-          mask = (1 << l) - 1;
-          inv_per = inv_small(per);
-          inv_w = inv_small(w);
-        }
-        const int loc = e - lbeg;
-        const int t = div_small(loc, inv_per);
-        const int rem = loc - t * per;
-        const int a = div_small(rem, inv_w);
-        const int bb = rem - a * w;
-        cp_async4(sDet + e, in + (((1 + t) << (2 * l)) + (((ys + a) & mask) << l) + ((xs + bb) & mask)));
-      }
-    };
-    load_range(m - 3, 0);                      // group A
-    cp_async_commit();
-    load_range(m - 1, m >= 2 ? m - 2 : m - 1); // group B
-    cp_async_commit();
-    cp_async_wait_group1();                    // A complete, B may be in flight
-  }
+  HS_PHASE(1)
+  // ---- detail windows in two cp.async groups: group A = ancestors' windows (levels <= m-3),
+  //      group B = the large windows of levels m-2 and m-1; the ancestors' top-down runs while
+  //      group B is still in flight.  Per level d = m - l the window side is a compile-time
+  //      constant, so the element decode uses constant divisors.
+  load_windows<G, 3, HS_MAX_LOG2N>(in, sDet, sR, sDoff, m);  // group A: d = 3 .. m
+  cp_async_commit();
+  if (m - 1 >= 2)
+    load_window_vec<G>(in, sDet, sR, sDoff, m);               // group B: d = 1 (16-byte chunks)
+  else
+    load_windows<G, 1, 1>(in, sDet, sR, sDoff, m);
+  load_windows<G, 2, 2>(in, sDet, sR, sDoff, m);             // group B: d = 2
+  cp_async_commit();
+  cp_async_wait_group1();                                    // A complete, B may be in flight
   __syncthreads();
 
+  HS_PHASE(2)
   // ---- (1) ancestors top-down: fields of levels 1 .. m-1 (level m-1 -> sB1, others alias sCh)
   auto ancestor_level = [&](int l) {
-    const int d = m - l;                      // parent window at level l: P(d)
     const int pw = sR[0][1][l];
     const int ys = sR[0][0][l], xs = sR[1][0][l];
     const int dw = pw + 1, dplane = dw * dw;
@@ -332,17 +332,23 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     }
     __syncthreads();
   };
+  HS_PHASE(3)
   for (int l = 0; l + 2 < m; ++l) ancestor_level(l);  // uses group A only
   cp_async_wait_all();
   __syncthreads();
+  HS_PHASE(4)
   if (m >= 2) ancestor_level(m - 2);                  // level m-1 fields (group B)
 
+  HS_PHASE(5)
   // ---- (1') level m-1 -> m, all three fields per parent, parity-split child planes
   {
     const int l = m - 1;
     const int ys = sR[0][0][l], xs = sR[1][0][l];
-    constexpr int DW = G::P1 + 1, DPL = DW * DW;
-    const float* dt = sDet + sDoff[l];
+    constexpr int DW = G::P1 + 1;
+    const bool vec = (m - 1 >= 2);                 // level m-1 window stored with padded rows
+    const int RW = vec ? G::WS1 : DW;              // row stride
+    const int DPL = DW * RW;                       // plane stride
+    const float* dt = sDet + sDoff[l] + (vec ? (sR[1][0][l] & 3) : 0);
     const FT asc = FT(pow2f(l));
     int poy = 0, pox = 0;
     if (l > 0) {
@@ -353,9 +359,9 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
 #pragma unroll 1
     for (int idx = tid; idx < NP; idx += kThreads) {
       const int pi = idx / G::P1, pj = idx - pi * G::P1;  // constant divisor
-      const int o = pi * DW + pj;
+      const int o = pi * RW + pj;
       FT H[4], V[4], D[4];  // cells (i,j), (i,j+1), (i+1,j), (i+1,j+1)
-      const int oo[4] = {o, o + 1, o + DW, o + DW + 1};
+      const int oo[4] = {o, o + 1, o + RW, o + RW + 1};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         H[q] = FT(dt[oo[q]]) * asc;
@@ -396,6 +402,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     __syncthreads();
   }
 
+  HS_PHASE(6)
   // ---- (2)+(3) fused shift + first bottom-up: register-sliding window down each thread's strip,
   //      taps at immediate offsets; shifted level-(m-1) fields -> sB1, owned outputs -> global
   {
@@ -463,6 +470,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     __syncthreads();
   }
 
+  HS_PHASE(7)
   // ---- (3) plain bottom-up for levels m-2 .. c (compile-time windows), sB1 <-> sCh
   const FT* srcS = sB1;
   int srcN = SN1, srcPlane = CB * CB;
@@ -506,6 +514,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   }
   // srcS holds the shifted level-c fields over the owned tile (srcN = TC when K >= 2; SN1 = TC when K = 1)
 
+  HS_PHASE(8)
   if (blockIdx.x == 0 && tid == 0) out[0] = __ldg(in);  // scaling coefficient: unchanged (R8)
   if (c == 0) return;
 
@@ -517,15 +526,15 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     const int ii = r / TC, jj = r - ii * TC;
     wsf[(long long)fld * gc * gc + (long long)(i0 + ii) * gc + (j0 + jj)] = srcS[fld * srcPlane + ii * srcN + jj];
   }
-  __threadfence();
-  __syncthreads();
+  __syncthreads();  // all of this CTA's field writes happen-before thread 0's release below
   if (tid == 0) {
-    const unsigned prev = atomicAdd(args.counters + g, 1u);
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(args.counters + g) : "memory");
     *sLast = (prev == (unsigned)(tpr * tpr - 1));
   }
-  __syncthreads();
+  __syncthreads();  // thread 0's acquire (other tiles' fields visible) orders the reads below
+  HS_PHASE(9)
   if (!*sLast) return;
-  __threadfence();
   const long long need = 3ll * gc * gc + 3ll * (gc / 2) * (gc / 2);
   if (need * (long long)sizeof(FT) <= (long long)S::BYTES) {
     FT* A = reinterpret_cast<FT*>(smem);
