@@ -54,6 +54,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunks", type=int, default=4)
     p.add_argument("--e2e-chunks", type=int, default=4)
+    p.add_argument("--start-level", type=int, default=None,
+                   help="coarse-start shift (row f4, approximate): shift the level-L approximation only")
     return p.parse_args()
 
 
@@ -230,6 +232,9 @@ def run_ours(args, cfg):
     full_out = world == 1
     shifted = torch.empty((B, F, N * N if full_out else kf), dtype=torch.float32, device=dev)
     ws = torch.empty(hs.haar_shift_workspace_bytes(2, n, F, B), dtype=torch.uint8, device=dev)
+    shifted_band = torch.empty((B, F, kf), dtype=torch.float32, device=dev) if args.start_level is not None else None
+    if args.start_level is not None and world > 1:
+        raise SystemExit("--start-level is a single-GPU option")
     R = torch.empty((rows, B), dtype=torch.float32, device=dev)
     R_full = torch.empty((V, B), dtype=torch.float32, device=dev) if (rank == 0 and world > 1) else None
     rws_bytes = hs.relight_workspace_bytes(F, kf, B)
@@ -256,7 +261,11 @@ def run_ours(args, cfg):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            hs.haar_shift_coeffs(light, shifts, 2, n if full_out else cfg.band_levels, out=shifted, workspace=ws)
+            if args.start_level is not None:
+                hs.haar_shift_coeffs_coarse(light, shifts, args.start_level, cfg.band_levels, out=shifted_band,
+                                            workspace=ws)
+            else:
+                hs.haar_shift_coeffs(light, shifts, 2, n if full_out else cfg.band_levels, out=shifted, workspace=ws)
             e1.record(stream)
             shift_events.append((e0, e1))
             launches["n"] += hs.last_launch_count()
@@ -264,7 +273,7 @@ def run_ours(args, cfg):
             hsdist.broadcast_band(shifted)
             _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
             return full
-        relight_fn(T, shifted, R)
+        relight_fn(T, shifted_band if args.start_level is not None else shifted, R)
         return R
 
     for _ in range(args.warmup):
@@ -382,6 +391,7 @@ def run_ours(args, cfg):
                          "traffic": traffic, "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes),
                          "avg_launch_ms": avg_ms, "share_of_step": sum(rel_ms) / args.steps / ms},
             "shift_ms": (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events)) if shift_events else None,
+            "shift_start_level": args.start_level,
             "shift_frac_hbm": ((2 * B * F * N * N * 4 if full_out else B * F * (N * N + kf) * 4) /
                                (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events) * 1e-3) / 1e9 / peak)
             if shift_events else None,

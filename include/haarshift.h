@@ -90,6 +90,29 @@ HS_API hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int lo
 HS_API size_t haar_shift_workspace_bytes(int ndim, int log2n, int faces, int batch);
 
 /* ---------------------------------------------------------------------------------------------
+ * haar_shift_coeffs_coarse -- coarse-start shift (R23).
+ *
+ * Defines:  P:520 ("one can start at any resolution level that is lower than n-1. In that case,
+ *           the computational complexity is reduced to O(N/4^k), where k is the number of levels
+ *           removed").  Computes the shift of the level-L approximation of each face: the HAAR1
+ *           prefix of levels < L (a 2^L x 2^L map of cell means) shifted by s / 2^(n-L) cells with
+ *           the same exact Haar-domain method, in O(4^L).  Equal to the exact shift's levels < L
+ *           when s is a multiple of 2^(n-L); an approximation of them otherwise (accuracy study:
+ *           tests/test_gpu_coarse.py).
+ *
+ *   in            [batch][faces][4^in_log2n] fp32 HAAR1 pyramids (only the prefix is read).
+ *   out           [batch][faces][4^band_levels], band_levels <= start_level.
+ *   in_log2n      1 .. HS_MAX_LOG2N;  start_level L: 1 .. in_log2n.
+ *   shifts_host   HOST [batch][faces][2] fp64 shifts in finest-pixel units (as haar_shift_coeffs).
+ *   workspace     >= haar_shift_coarse_workspace_bytes(...).
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status haar_shift_coeffs_coarse(const float* in, float* out, int in_log2n, int start_level, int faces,
+                                          int batch, const double* shifts_host, int band_levels,
+                                          void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t haar_shift_coarse_workspace_bytes(int in_log2n, int start_level, int faces, int batch);
+
+/* ---------------------------------------------------------------------------------------------
  * relight_vertices -- per-vertex light-transport inner product.
  *
  * Defines:  eq:tripleSum P:253-266 with the Tripling Coefficient Theorem's scaling case

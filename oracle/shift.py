@@ -73,6 +73,19 @@ def shift_coeffs2d(c: np.ndarray, sy: float, sx: float) -> np.ndarray:
     return haar.forward2d(shift_pixels2d(haar.inverse2d(c), sy, sx))
 
 
+def shift_coeffs_coarse2d(c: np.ndarray, start_level: int, sy: float, sx: float) -> np.ndarray:
+    """Coarse start ("one can start at any resolution level that is lower than n-1 ...
+    the computational complexity is reduced to O(N/4^k)"), reading R23: the shift of the
+    level-L approximation.  Keep the HAAR1 prefix of levels < L (4**L coefficients), synthesise it
+    at 2**L x 2**L (each cell the mean of its 2**(n-L) x 2**(n-L) pixels), box-project-shift that
+    map by s / 2**(n-L) cells, forward transform.  Returns the 4**L coefficients (levels < L)."""
+    c = np.asarray(c, dtype=np.float64).reshape(-1)
+    n = haar.log2_exact(int(round(np.sqrt(c.size))))
+    k = n - start_level
+    prefix = c[: 4 ** start_level]
+    return shift_coeffs2d(prefix, sy / 2.0 ** k, sx / 2.0 ** k)
+
+
 def shift_coeffs(coeffs: np.ndarray, shifts: np.ndarray, ndim: int, band_levels: int | None = None):
     """Batched: coeffs [batch][faces][N**ndim... flattened], shifts [batch][faces][ndim] ->
     shifted pyramids (fp64), optionally truncated to the HAAR1 prefix holding the scaling and

@@ -15,7 +15,9 @@ from __future__ import annotations
 
 from ._lib import HaarShiftError, load  # noqa: F401
 from .api import (  # noqa: F401
+    haar_shift_coarse_workspace_bytes,
     haar_shift_coeffs,
+    haar_shift_coeffs_coarse,
     haar_shift_workspace_bytes,
     hs_fill_transfer,
     last_launch_count,
@@ -27,7 +29,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_workspace_bytes", "hs_fill_transfer",
+    "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_coeffs_coarse", "haar_shift_coarse_workspace_bytes", "haar_shift_workspace_bytes", "hs_fill_transfer",
     "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
     "shift_and_relight",
 ]

@@ -77,6 +77,34 @@ def haar_shift_coeffs(coeffs: torch.Tensor, shifts, ndim: int = 2, band_levels: 
     return out
 
 
+def haar_shift_coarse_workspace_bytes(in_log2n: int, start_level: int, faces: int, batch: int) -> int:
+    return int(load().haar_shift_coarse_workspace_bytes(in_log2n, start_level, faces, batch))
+
+
+def haar_shift_coeffs_coarse(coeffs: torch.Tensor, shifts, start_level: int, band_levels: Optional[int] = None,
+                             out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Coarse-start shift: coeffs [batch][faces][4**n] -> the shifted level-L approximation,
+    [batch][faces][4**band] (band <= L, default L).  shifts: host [batch][faces][2] in pixels."""
+    lib = load()
+    _dev_f32(coeffs, "coeffs")
+    B, F, K = coeffs.shape
+    n = (int(K).bit_length() - 1) // 2
+    band = start_level if band_levels is None else int(band_levels)
+    sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(B, F, 2))
+    if out is None:
+        out = torch.empty((B, F, 4 ** band), dtype=torch.float32, device=coeffs.device)
+    _dev_f32(out, "out")
+    need = haar_shift_coarse_workspace_bytes(n, start_level, F, B)
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
+    st = lib.haar_shift_coeffs_coarse(coeffs.data_ptr(), out.data_ptr(), n, start_level, F, B,
+                                      sh.ctypes.data_as(ctypes.c_void_p), band,
+                                      workspace.data_ptr() if need else None, need, _stream_ptr(stream))
+    check("haar_shift_coeffs_coarse", st)
+    return out
+
+
 def relight_workspace_bytes(faces: int, k_face: int, batch: int) -> int:
     return int(load().relight_workspace_bytes(faces, k_face, batch))
 

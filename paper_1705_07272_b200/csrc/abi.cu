@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -110,8 +111,42 @@ hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, in
   if (!aligned16(in) || !aligned16(out) || (need > 0 && !aligned16(workspace))) return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
   if (s != HS_OK) return s;
-  s = launch_shift(in, out, ndim, log2n, faces, nfaces, (long long)faces * (long long)K, shifts_host, nullptr,
-                   nullptr, band_levels, workspace, workspace_bytes, (cudaStream_t)stream);
+  s = launch_shift(in, out, ndim, log2n, faces, nfaces, (long long)faces * (long long)K, (long long)K, shifts_host,
+                   nullptr, nullptr, band_levels, workspace, workspace_bytes, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+size_t haar_shift_coarse_workspace_bytes(int in_log2n, int start_level, int faces, int batch) {
+  if (in_log2n < 1 || in_log2n > HS_MAX_LOG2N || start_level < 1 || start_level > in_log2n) return 0;
+  return haar_shift_workspace_bytes(2, start_level, faces, batch);
+}
+
+hs_status haar_shift_coeffs_coarse(const float* in, float* out, int in_log2n, int start_level, int faces, int batch,
+                                   const double* shifts_host, int band_levels, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!in || !out || !shifts_host) return HS_ERR_INVALID_ARG;
+  if (in_log2n < 1 || in_log2n > HS_MAX_LOG2N || start_level < 1 || start_level > in_log2n) return HS_ERR_INVALID_ARG;
+  if (faces < 1 || batch < 1 || band_levels < 0 || band_levels > start_level) return HS_ERR_INVALID_ARG;
+  const long long nfaces = (long long)faces * batch;
+  for (long long i = 0; i < nfaces * 2; ++i)
+    if (!std::isfinite(shifts_host[i])) return HS_ERR_INVALID_ARG;
+  const size_t K = (size_t)1 << (2 * in_log2n);
+  const size_t Kb = (size_t)1 << (2 * band_levels);
+  if (overlap(in, nfaces * K * 4, out, nfaces * Kb * 4)) return HS_ERR_INVALID_ARG;
+  const size_t need = shift_workspace_bytes_impl(2, start_level, nfaces);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(in) || !aligned16(out) || (need > 0 && !aligned16(workspace))) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  // the level-L approximation is the HAAR1 prefix; a shift of s pixels moves it by s / 2^(n-L) cells
+  std::vector<double> sc((size_t)nfaces * 2);
+  const double inv = std::ldexp(1.0, -(in_log2n - start_level));
+  for (size_t i = 0; i < sc.size(); ++i) sc[i] = shifts_host[i] * inv;
+  s = launch_shift(in, out, 2, start_level, faces, nfaces, (long long)faces * (long long)K, (long long)K, sc.data(),
+                   nullptr, nullptr, band_levels, workspace, workspace_bytes, (cudaStream_t)stream);
   g_last_launches = g_launches;
   return s;
 }
@@ -185,8 +220,8 @@ hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, 
   float* S = reinterpret_cast<float*>(base + shift_ws + fpb);
   for (long long v0 = 0; v0 < num_vertices; v0 += vc) {
     const long long nv = (num_vertices - v0) < vc ? (num_vertices - v0) : vc;
-    s = launch_shift(light, S, 2, log2n, faces, nv * faces, 0, nullptr, vertex_shifts + 2 * v0, fp, log2n,
-                     workspace, shift_ws, st);
+    s = launch_shift(light, S, 2, log2n, faces, nv * faces, 0, 1ll << (2 * log2n), nullptr, vertex_shifts + 2 * v0,
+                     fp, log2n, workspace, shift_ws, st);
     if (s != HS_OK) break;
     s = launch_rowdot(transfer + v0 * K, S, nv, K, radiance + v0, st);
     if (s != HS_OK) break;

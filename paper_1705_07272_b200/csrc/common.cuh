@@ -115,6 +115,7 @@ struct ShiftArgs {
   unsigned* counters;         // per-face tile-completion counters (zeroed before launch)
   const FaceParam* dev_fp;    // device FaceParams (per-vertex path) or nullptr -> use fp[]
   long long in_batch_stride;  // elements; 0 broadcasts one pyramid set to every batch entry
+  long long in_face_stride;   // elements between the faces of one batch entry (>= K)
   long long ws_face_stride;   // floats per face in ws
   int log2n, faces, band, out_face_stride, num_faces;
   FaceParam fp[kMaxFacesPerLaunch];
@@ -135,7 +136,8 @@ inline long long ws_face_floats_2d(int n) {  // elements of the field type per f
 
 size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces);
 hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int faces,
-                       long long num_faces, long long in_batch_stride, const double* shifts_host,
+                       long long num_faces, long long in_batch_stride, long long in_face_stride,
+                       const double* shifts_host,
                        const float* shifts_dev_per_vertex, FaceParam* dev_fp_buf, int band,
                        void* ws, size_t ws_bytes, cudaStream_t st);
 

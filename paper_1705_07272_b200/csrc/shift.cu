@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
   const int n = args.log2n, N = 1 << n;
   const int m = P.m;
   const int b = g / args.faces, f = g % args.faces;
-  const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * N;
+  const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const int band = args.band;
   const int Kb = 1 << band;
@@ -113,7 +113,8 @@ size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces) {
 
 // in:  [num_faces / faces batches][faces][K]; out [num_faces][Kb]
 hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int faces,
-                       long long num_faces, long long in_batch_stride, const double* shifts_host,
+                       long long num_faces, long long in_batch_stride, long long in_face_stride,
+                       const double* shifts_host,
                        const float* shifts_dev_per_vertex, FaceParam* dev_fp_buf, int band,
                        void* ws, size_t ws_bytes, cudaStream_t st) {
   const int n = log2n;
@@ -144,6 +145,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     a.counters = counters ? counters + g0 : nullptr;
     a.dev_fp = nullptr;
     a.in_batch_stride = in_batch_stride;
+    a.in_face_stride = in_face_stride;
     a.ws_face_stride = wsface;
     a.log2n = n;
     a.faces = faces;

@@ -222,7 +222,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   const int n = args.log2n;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in =
-      args.in + (long long)b * args.in_batch_stride + (long long)f * ((long long)1 << (2 * n));
+      args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const int band = args.band;
   const int tid = threadIdx.x;
@@ -594,7 +594,7 @@ __global__ void permute_kernel(const __grid_constant__ ShiftArgs args) {
   if (m >= args.band && m != 0) return;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in =
-      args.in + (long long)b * args.in_batch_stride + (long long)f * ((long long)1 << (2 * n));
+      args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const long long lo = (m == 0) ? 0 : (1ll << (2 * m));
   const long long hi = 1ll << (2 * args.band);

@@ -184,3 +184,39 @@ def test_batched_and_band():
     np.testing.assert_allclose(out[1, 2], shift.shift_coeffs2d(c[1, 2], *s[1, 2]))
     band = shift.shift_coeffs(c, s, 2, band_levels=2)
     np.testing.assert_array_equal(band, out[:, :, :16])
+
+
+# ----------------------------------------------------------------- coarse start (f4, R23)
+
+def test_coarse_start_is_exact_for_dyadic_shifts():
+    """Shifts that are multiples of 2**(n-L) move the level-L approximation by whole cells, so the
+    coarse start reproduces the exact shift's levels < L (SPEC.md S:277 permutation argument)."""
+    n, N = 5, 32
+    c = np.random.default_rng(20).normal(size=N * N)
+    for L in (2, 3, 4):
+        step = 2 ** (n - L)
+        for q in [(step, 0), (3 * step, 2 * step), (0, 5 * step), (-step, 7 * step)]:
+            exact = shift.shift_coeffs2d(c, *q)[: 4 ** L]
+            np.testing.assert_allclose(shift.shift_coeffs_coarse2d(c, L, *q), exact, atol=1e-12)
+
+
+def test_coarse_start_at_full_level_is_the_exact_shift():
+    c = np.random.default_rng(21).normal(size=256)
+    for s in [(0.3, 7.25), (-3.5, 1.0)]:
+        np.testing.assert_allclose(shift.shift_coeffs_coarse2d(c, 4, *s), shift.shift_coeffs2d(c, *s), atol=1e-12)
+
+
+def test_coarse_start_equals_shift_of_truncated_map_cells():
+    """Independent restatement: the level-L cells are the means of 2**k x 2**k pixel blocks; shift
+    that block-mean image by s/2**k with the brute-force Fraction operator of tests/brute.py."""
+    n, L = 3, 2
+    N = 1 << n
+    f = np.random.default_rng(22).integers(-5, 6, size=(N, N)).astype(float)
+    P = brute.basis2d(n)
+    c = P @ f.ravel() / (N * N)
+    cells = f.reshape(4, 2, 4, 2).mean(axis=(1, 3))                  # level-2 approximation
+    P2 = brute.basis2d(L)
+    c2 = [Fraction(x).limit_denominator(1 << 20) for x in P2 @ cells.ravel() / 16]
+    M = brute.overlap_shift_matrix_2d(L, Fraction(3, 4), Fraction(-5, 4))   # s / 2 = (0.75, -1.25)
+    expect = np.array([float(x) for x in brute.apply_fraction_matrix(M, c2)])
+    np.testing.assert_allclose(shift.shift_coeffs_coarse2d(c, L, 1.5, -2.5), expect, atol=1e-13)
