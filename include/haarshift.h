@@ -164,6 +164,34 @@ HS_API hs_status relight_vertices_shifted(const float* transfer, int64_t num_ver
 HS_API size_t relight_shifted_workspace_bytes(int64_t num_vertices, int faces, int log2n);
 
 /* ---------------------------------------------------------------------------------------------
+ * relight_vertices_sparse -- relight with sparse (top-K) transfer vectors.
+ *
+ * Defines:  P:240-245 (non-linear wavelet approximation: keep the largest coefficients of the
+ *           transfer), eq:tripleSum P:253-266 with C_{ij0} = delta_ij: the double product
+ *           over the kept coefficients only.
+ *
+ *   radiance[v][b] = sum_{k < k_sparse} values[v][k] * light[b][indices[v][k]]
+ *   indices       DEVICE [num_vertices][k_sparse] int32 in [0, total_coeffs) (duplicates add).
+ *   values        DEVICE [num_vertices][k_sparse] fp32.
+ *   light         DEVICE [batch][total_coeffs] fp32 (e.g. full shifted pyramids, faces concatenated).
+ *   radiance      DEVICE [num_vertices][batch] fp32.
+ *   workspace     >= relight_sparse_workspace_bytes(total_coeffs, batch): the light transposed to
+ *                 coefficient-major [total_coeffs][batch] (one contiguous row per gathered index).
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status relight_vertices_sparse(const int32_t* indices, const float* values, int64_t num_vertices,
+                                         int k_sparse, const float* light, int64_t total_coeffs, int batch,
+                                         float* radiance, void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t relight_sparse_workspace_bytes(int64_t total_coeffs, int batch);
+
+/* Seeded sparse transfer rows, bit-identical to synth.sparse_transfer_rows (input generator):
+ * per vertex the first faces * 4^dense_levels pairs are every face's levels < dense_levels, the
+ * rest hash-drawn detail coefficients; values u * 2^-level (|u| for scaling).                   */
+HS_API hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_t row_start, int64_t row_count,
+                                         int faces, int log2n, int k_sparse, int dense_levels, uint64_t seed,
+                                         void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * hs_fill_transfer -- seeded synthetic transfer rows, generated in place (input generator, not
  * part of the method; bit-identical to synth.transfer_rows):
  *   T[v][f*k_face + k] = u * 2^-level(k), u = ((h >> 40) - 2^23) / 2^23,

@@ -31,6 +31,18 @@ def relight(transfer: np.ndarray, light: np.ndarray, faces: int, k_face: int) ->
     return T @ band.T
 
 
+def relight_sparse(idx: np.ndarray, val: np.ndarray, light: np.ndarray) -> np.ndarray:
+    """Sparse transfer (non-linear approximation): vertex v keeps
+    K_s coefficients (idx[v][k] into the concatenated per-face pyramids, val[v][k]); the double
+    product is R[v][b] = sum_k val[v][k] * light[b][idx[v][k]]  (light [B][faces*N*N], fp64)."""
+    L = np.asarray(light, dtype=np.float64).reshape(np.asarray(light).shape[0], -1)
+    vals = np.asarray(val, dtype=np.float64)
+    out = np.empty((vals.shape[0], L.shape[0]), dtype=np.float64)
+    for v in range(vals.shape[0]):
+        out[v] = L[:, np.asarray(idx[v], dtype=np.int64)] @ vals[v]
+    return out
+
+
 def relight_shifted(transfer: np.ndarray, light: np.ndarray, vertex_shifts: np.ndarray) -> np.ndarray:
     """transfer [V][faces*N*N], light [faces][N*N] (one full pyramid per face), vertex_shifts
     [V][2] (sy, sx), the same shift for every face of a vertex -> radiance [V] (fp64)."""

@@ -19,17 +19,21 @@ from .api import (  # noqa: F401
     haar_shift_coeffs,
     haar_shift_coeffs_coarse,
     haar_shift_workspace_bytes,
+    hs_fill_sparse_transfer,
     hs_fill_transfer,
     last_launch_count,
     relight_shifted_workspace_bytes,
     relight_vertices,
     relight_workspace_bytes,
+    relight_sparse_workspace_bytes,
     relight_vertices_shifted,
+    relight_vertices_sparse,
     shift_and_relight,
 )
 
 __all__ = [
     "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_coeffs_coarse", "haar_shift_coarse_workspace_bytes", "haar_shift_workspace_bytes", "hs_fill_transfer",
     "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
-    "shift_and_relight",
+    "shift_and_relight", "hs_fill_sparse_transfer", "relight_vertices_sparse",
+    "relight_sparse_workspace_bytes",
 ]

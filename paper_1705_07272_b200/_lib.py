@@ -27,6 +27,11 @@ SIGNATURES = {
     "relight_shifted_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int, _c.c_int]),
     "hs_fill_transfer": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_int, _c.c_uint64,
                                     _c.c_uint64, _c.c_void_p]),
+    "relight_vertices_sparse": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_void_p, _c.c_int64,
+                                           _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "relight_sparse_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int]),
+    "hs_fill_sparse_transfer": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_int,
+                                           _c.c_int, _c.c_int, _c.c_uint64, _c.c_void_p]),
     "hs_last_launch_count": (_c.c_int, []),
     "hs_status_string": (_c.c_char_p, [_c.c_int]),
     "hs_last_cuda_error": (_c.c_char_p, []),

@@ -164,6 +164,44 @@ def relight_vertices_shifted(transfer: torch.Tensor, light: torch.Tensor, vertex
     return out
 
 
+def relight_sparse_workspace_bytes(total_coeffs: int, batch: int) -> int:
+    return int(load().relight_sparse_workspace_bytes(total_coeffs, batch))
+
+
+def relight_vertices_sparse(indices: torch.Tensor, values: torch.Tensor, light: torch.Tensor,
+                            out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """indices int32 / values fp32 [V][K_s], light [batch][...] (flattened to [batch][C]) -> [V][batch]."""
+    lib = load()
+    if indices.dtype != torch.int32 or not indices.is_cuda or not indices.is_contiguous():
+        raise TypeError("indices must be a contiguous CUDA int32 tensor")
+    _dev_f32(values, "values")
+    _dev_f32(light, "light")
+    V, ks = indices.shape
+    B = light.shape[0]
+    C = light.numel() // B
+    if out is None:
+        out = torch.empty((V, B), dtype=torch.float32, device=values.device)
+    need = relight_sparse_workspace_bytes(C, B)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=values.device)
+    st = lib.relight_vertices_sparse(indices.data_ptr(), values.data_ptr(), V, ks, light.data_ptr(), C, B,
+                                     out.data_ptr(), workspace.data_ptr(), need, _stream_ptr(stream))
+    check("relight_vertices_sparse", st)
+    return out
+
+
+def hs_fill_sparse_transfer(indices: torch.Tensor, values: torch.Tensor, row_start: int, faces: int, log2n: int,
+                            dense_levels: int, seed: int, stream: Optional[torch.cuda.Stream] = None):
+    """Fill indices/values [rows][K_s] with synth.sparse_transfer_rows (bit for bit)."""
+    lib = load()
+    rows, ks = indices.shape
+    st = lib.hs_fill_sparse_transfer(indices.data_ptr(), values.data_ptr(), row_start, rows, faces, log2n, ks,
+                                     dense_levels, seed % 2**64, _stream_ptr(stream))
+    check("hs_fill_sparse_transfer", st)
+    return indices, values
+
+
 def hs_fill_transfer(out: torch.Tensor, row_start: int, faces: int, k_face: int, seed: int, stream_id: int,
                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """Fill out [rows][faces*k_face] with the seeded synthetic transfer rows (synth.transfer_rows)."""

@@ -230,6 +230,46 @@ hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, 
   return s;
 }
 
+size_t relight_sparse_workspace_bytes(int64_t total_coeffs, int batch) {
+  if (total_coeffs < 1 || batch < 1 || batch > 1024) return 0;
+  return (size_t)total_coeffs * (size_t)batch * sizeof(float);
+}
+
+hs_status relight_vertices_sparse(const int32_t* indices, const float* values, int64_t num_vertices, int k_sparse,
+                                  const float* light, int64_t total_coeffs, int batch, float* radiance,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!indices || !values || !light || !radiance || !workspace) return HS_ERR_INVALID_ARG;
+  if (num_vertices < 1 || k_sparse < 1 || total_coeffs < 1 || total_coeffs >= (1ll << 31)) return HS_ERR_INVALID_ARG;
+  if (batch < 1 || batch > 1024) return HS_ERR_INVALID_ARG;
+  if (workspace_bytes < relight_sparse_workspace_bytes(total_coeffs, batch)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(indices) || !aligned16(values) || !aligned16(light) || !aligned16(radiance) || !aligned16(workspace))
+    return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_relight_sparse(indices, values, num_vertices, k_sparse, light, total_coeffs, batch, radiance,
+                            reinterpret_cast<float*>(workspace), (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_t row_start, int64_t row_count, int faces,
+                                  int log2n, int k_sparse, int dense_levels, uint64_t seed, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!indices || !values || row_start < 0 || row_count < 1 || faces < 1) return HS_ERR_INVALID_ARG;
+  if (log2n < 1 || log2n > HS_MAX_LOG2N || dense_levels < 0 || dense_levels > log2n) return HS_ERR_INVALID_ARG;
+  if (k_sparse < (faces << (2 * dense_levels)) || (long long)faces << (2 * log2n) >= (1ll << 31)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(indices) || !aligned16(values)) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_fill_sparse(indices, values, row_start, row_count, faces, log2n, k_sparse, dense_levels, seed,
+                         (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
 hs_status hs_fill_transfer(float* out, int64_t row_start, int64_t row_count, int faces, int k_face,
                            uint64_t seed, uint64_t stream_id, void* stream) {
   g_last_launches = 0;

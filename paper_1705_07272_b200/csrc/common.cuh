@@ -152,6 +152,10 @@ bool relight_shifted_fused_supported(int log2n);
 size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n);
 hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, const float* light, int log2n,
                                        const float* shifts, float* R, void* ws, cudaStream_t st);
+hs_status launch_fill_sparse(int* idx, float* val, long long row_start, long long rows, int faces, int n, int ks,
+                             int dense_levels, uint64_t seed, cudaStream_t st);
+hs_status launch_relight_sparse(const int* idx, const float* val, long long V, int ks, const float* light, long long C,
+                                int B, float* R, float* Lt, cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
                                int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
 

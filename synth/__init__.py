@@ -104,6 +104,48 @@ def transfer_rows(seed: int, row_start: int, row_count: int, faces: int, k_face:
     return t.astype(np.float32)
 
 
+STREAM_TS = 0x5A12              # counter-hash stream of the sparse transfer
+
+
+def sparse_transfer_rows(seed: int, row_start: int, row_count: int, faces: int, log2n: int, k_sparse: int,
+                         dense_levels: int = 2):
+    """Sparse per-vertex transfer (non-linear approximation):
+    K_s (index, value) pairs per vertex over the full pyramids of `faces` faces (index in
+    [0, faces * 4**n)).  The first faces * 4**dense_levels entries are every face's coefficients of
+    levels < dense_levels (scaling included); the others are hash-drawn detail coefficients with a
+    level uniform in [dense_levels, n), a type and a cell.  Values u * 2**-level (|u| for scaling),
+    u from hash_uniform.  Returns (idx int32 [rows][K_s], val fp32 [rows][K_s]); csrc/fill.cu's
+    hs_fill_sparse_transfer reproduces both bit for bit."""
+    N2 = 4 ** log2n
+    nd = faces * 4 ** dense_levels
+    if k_sparse < nd:
+        raise ValueError("k_sparse must cover the dense coarse levels")
+    v = np.arange(row_start, row_start + row_count, dtype=np.uint64)[:, None]
+    k = np.arange(k_sparse, dtype=np.uint64)[None, :]
+    gi = v * np.uint64(k_sparse) + k
+    h = hash_u64(seed, STREAM_TS, gi)
+    kk = np.broadcast_to(np.arange(k_sparse, dtype=np.int64)[None, :], gi.shape)
+    # dense part
+    f_d = kk // (4 ** dense_levels)
+    c_d = kk % (4 ** dense_levels)
+    # hashed part: level, type, cell, face from independent bit fields of h
+    nlev = log2n - dense_levels
+    lev = dense_levels + ((h >> np.uint64(8)) % np.uint64(max(nlev, 1))).astype(np.int64)
+    typ = ((h >> np.uint64(16)) % np.uint64(3)).astype(np.int64)
+    face = ((h >> np.uint64(24)) % np.uint64(faces)).astype(np.int64)
+    cell = ((h >> np.uint64(32)) & np.uint64(0xFFFFFFFF)).astype(np.int64) % (4 ** lev)
+    c_h = (4 ** lev) * (1 + typ) + cell
+    dense = kk < nd
+    coef = np.where(dense, c_d, c_h)
+    fidx = np.where(dense, f_d, face)
+    idx = (fidx * N2 + coef).astype(np.int32)
+    lvl = np.where(coef == 0, 0, level_of_index_2d(coef))
+    u = hash_uniform(seed, STREAM_T, gi)
+    val = (u * np.ldexp(np.float32(1.0), -lvl).astype(np.float32)).astype(np.float32)
+    val = np.where(coef == 0, np.abs(val), val).astype(np.float32)
+    return idx, val
+
+
 def _sun_params(rng: np.random.Generator, n: int, suns: int):
     N = 1 << n
     r = rng.integers(0, N, size=suns)
@@ -237,6 +279,9 @@ CONFIGS = {
     "c3": Config("c3", 6, 6, 10000, 6, 1, SEED_BASE + 3, "6x64x64 cube map, 10k vertices, per-frame global shift + relight"),
     "c4": Config("c4", 7, 6, 100000, 7, 1, SEED_BASE + 4, "6x128x128 cube map, 100k vertices, per-vertex shifts"),
     "c5": Config("c5", 8, 6, 1000000, 5, 64, SEED_BASE + 5, "6x256x256 cube map, 1M vertices, 64 frames"),
+    "c5s": Config("c5s", 8, 6, 1000000, 8, 64, SEED_BASE + 5,
+                  "c5 with sparse top-K transfer (K_s = 256 full-resolution coefficients per vertex, row f2)",
+                  {"k_sparse": 256, "dense_levels": 2}),
 }
 
 

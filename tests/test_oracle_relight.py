@@ -70,6 +70,34 @@ def test_relight_shifted_matches_loop():
     np.testing.assert_allclose(relight.relight_shifted(T, L, np.zeros((4, 2))), T @ L.reshape(-1), atol=1e-12)
 
 
+def test_sparse_relight_equals_dense_scatter():
+    """The sparse double product equals the dense one with the (idx, val) pairs scattered into a
+    dense transfer row (duplicates add), computed with BLAS."""
+    n, F, B = 4, 6, 3
+    idx, val = synth.sparse_transfer_rows(9, 0, 50, F, n, 120)
+    L = synth.light_pyramids(10, B, F, n).reshape(B, -1)
+    dense = np.zeros((50, F * 4 ** n))
+    for v in range(50):
+        np.add.at(dense[v], idx[v].astype(np.int64), val[v].astype(np.float64))
+    np.testing.assert_allclose(relight.relight_sparse(idx, val, L), dense @ L.T.astype(np.float64), rtol=1e-12,
+                               atol=1e-12)
+
+
+def test_sparse_generator_structure():
+    n, F, K = 5, 6, 200
+    idx, val = synth.sparse_transfer_rows(11, 3, 20, F, n, K, dense_levels=2)
+    assert idx.dtype == np.int32 and val.dtype == np.float32
+    assert idx.min() >= 0 and idx.max() < F * 4 ** n
+    dense_part = idx[:, :F * 16]
+    np.testing.assert_array_equal(dense_part, np.broadcast_to(
+        (np.arange(F)[:, None] * 4 ** n + np.arange(16)[None, :]).reshape(-1), dense_part.shape))
+    coef = idx % 4 ** n
+    lev = synth.level_of_index_2d(coef)
+    assert np.all(np.abs(val) <= 2.0 ** -lev)
+    assert np.all(val[coef == 0] >= 0)
+    np.testing.assert_array_equal(synth.sparse_transfer_rows(11, 5, 4, F, n, K)[0], idx[2:6])
+
+
 def test_synth_transfer_is_counter_based_and_exact():
     """Generator determinism: row subsets equal slices of the full matrix; values exact fp32."""
     full = synth.transfer_rows(123, 0, 20, 6, 16)
