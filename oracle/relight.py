@@ -12,6 +12,10 @@ is plugged in the triple integral computation").
 * ``relight``:          R[v][b] = sum_f sum_{k<K_face} T[v][f K_face + k] L'[b][f][k]
 * ``relight_shifted``:  r_v = < S_{s_v} L , T_v >, the shifted pyramid built per vertex by
                         inverse -> shift -> forward (shift.py); the inverse is shared.
+* ``relight_triple``:   the full triple product with BRDF and visibility
+                        kept separate: R[v][b] = sum_f integral of L'_b,f * rho_v,f * V_v,f, the
+                        integral eq:tripleSum abbreviates, evaluated by brute force
+                        on the pixels of the truncated pyramids.
 """
 from __future__ import annotations
 
@@ -19,7 +23,7 @@ import numpy as np
 
 from . import haar, shift
 
-__all__ = ["relight", "relight_shifted"]
+__all__ = ["relight", "relight_shifted", "relight_sparse", "relight_triple"]
 
 
 def relight(transfer: np.ndarray, light: np.ndarray, faces: int, k_face: int) -> np.ndarray:
@@ -58,4 +62,38 @@ def relight_shifted(transfer: np.ndarray, light: np.ndarray, vertex_shifts: np.n
             shifted = haar.forward2d(shift.shift_pixels2d(pixels[f], sy, sx))
             acc += float(np.dot(shifted, T[v, f * K:(f + 1) * K]))
         out[v] = acc
+    return out
+
+
+def _cells(prefix_rows: np.ndarray, k: int) -> np.ndarray:
+    """[rows][4**k] HAAR1 prefixes (levels < k) -> [rows][4**k] cell values of the 2**k x 2**k
+    piecewise-constant functions they represent (the prefix is itself a complete level-k pyramid
+    in the unit-square normalisation, R1)."""
+    rows = np.asarray(prefix_rows, dtype=np.float64)
+    return np.stack([haar.inverse2d(r).reshape(-1) for r in rows]) if rows.shape[0] else rows.copy()
+
+
+def relight_triple(brdf: np.ndarray, vis: np.ndarray, light: np.ndarray, faces: int, k_face: int) -> np.ndarray:
+    """brdf, vis [V][faces*k_face] (HAAR1 prefixes, k_face = 4**k), light [B][faces][>= k_face]
+    -> radiance [V][B], fp64:
+
+        R[v][b] = sum_f  integral over the unit square of  L_bf * rho_vf * V_vf
+                = sum_f  mean over the 4**k cells of the product of the three reconstructions.
+
+    This is the triple integral of eq:tripleSum before it is expanded into the sum
+    sum_ijk C_ijk a_i b_j c_k; the tests pin it to that sum with C_ijk integrated from the basis
+    table, and to the Tripling Coefficient Theorem's cases."""
+    k = int(round(np.log2(k_face) / 2))
+    if 4 ** k != k_face:
+        raise ValueError("k_face must be a power of 4")
+    rho = np.asarray(brdf, dtype=np.float64)
+    vv = np.asarray(vis, dtype=np.float64)
+    L = np.asarray(light, dtype=np.float64)
+    V, B = rho.shape[0], L.shape[0]
+    out = np.zeros((V, B), dtype=np.float64)
+    for f in range(faces):
+        sl = slice(f * k_face, (f + 1) * k_face)
+        prod = _cells(rho[:, sl], k) * _cells(vv[:, sl], k)          # [V][cells]
+        lc = _cells(L[:, f, :k_face], k)                              # [B][cells]
+        out += prod @ lc.T / k_face
     return out
