@@ -192,6 +192,48 @@ HS_API hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_
                                          void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * relight_vertices_triple -- triple-product relight, BRDF and visibility separate (SURVEY.md
+ * §8(f) f3).
+ *
+ * Defines:  eq:tripleSum P:253-266  R = sum_ijk C_ijk a_i b_j c_k  with a = light, b = BRDF,
+ *           c = visibility and C_ijk the integral of three basis functions, evaluated through the
+ *           Tripling Coefficient Theorem P:287-294 (cases (a), (b), (c)); per face:
+ *
+ *   radiance[v][b] = sum_f  integral over the unit square of  L_bf * rho_vf * V_vf
+ *
+ *   with every function truncated to its HAAR1 prefix of k_face = 4^k coefficients (levels < k).
+ *   brdf_q, vis_q  DEVICE [num_vertices][faces * k_face] fp32 in the qtree layout
+ *                  (haar_pack_qtree below).
+ *   light          DEVICE [batch][faces][light_face_stride] fp32 in HAAR1 order (the first k_face
+ *                  entries of each face are used -- e.g. the band written by haar_shift_coeffs).
+ *   radiance       DEVICE [num_vertices][batch] fp32.
+ *   k_face         4^k with 3 <= k <= 12.
+ *   workspace      >= relight_triple_workspace_bytes(...), 1024-byte aligned (HS_ERR_ALIGNMENT).
+ *   Precision: fp32 inputs; the tripling terms are formed in fp32 and multiplied on the tensor
+ *   cores in split fp16 (hi + 2^-11 lo) with fp32 accumulation when batch % 64 == 0 (DESIGN.md
+ *   §5.8), otherwise on CUDA cores in fp32.
+ *
+ * haar_pack_qtree -- HAAR1 -> qtree layout (the storage format of brdf_q / vis_q):
+ *   in   DEVICE [rows][faces][in_face_stride] fp32, HAAR1 prefix of 4^log2k used per face;
+ *   out  DEVICE [rows][faces][4^log2k] fp32.  With r = log2k - 3, face f of row v is 4^r chunks
+ *   of 64: chunk c (level-r cell (ci, cj) = (c >> r, c & (2^r - 1))) holds, for q = 0..3 (child
+ *   cell (2ci + q/2, 2cj + q%2) at level r+1) and p = 0..3 (grandchild (2i1 + p/2, 2j1 + p%2) at
+ *   level r+2): slot 15q + 3p + t = grandchild coefficient of type t (H, V, D); slot 15q + 12 + t
+ *   = child coefficient of type t; slot 60 + t = coefficient of cell c itself at level r; slot 63
+ *   = the mean of the function over cell c (scaling + the coarser levels evaluated on c).  The
+ *   layout holds the same information as the HAAR1 prefix (the 4^r cell means determine the
+ *   levels < r).  log2k >= 3; in and out must not overlap.
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status relight_vertices_triple(const float* brdf_q, const float* vis_q, int64_t num_vertices, int faces,
+                                         int k_face, const float* light, int64_t light_face_stride, int batch,
+                                         float* radiance, void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t relight_triple_workspace_bytes(int64_t num_vertices, int faces, int k_face, int batch);
+
+HS_API hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64_t in_face_stride, int log2k,
+                                 float* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * hs_fill_transfer -- seeded synthetic transfer rows, generated in place (input generator, not
  * part of the method; bit-identical to synth.transfer_rows):
  *   T[v][f*k_face + k] = u * 2^-level(k), u = ((h >> 40) - 2^23) / 2^23,

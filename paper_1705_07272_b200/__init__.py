@@ -7,6 +7,10 @@ device memory and streams.  Function names follow the C ABI:
 * ``haar_shift_coeffs``        shifted Haar pyramids, computed in the Haar domain
 * ``relight_vertices``         per-vertex transfer inner products (a6)
 * ``relight_vertices_shifted`` fused per-vertex shift + relight (a7)
+* ``relight_vertices_sparse``  relight with sparse top-K transfer (f2)
+* ``relight_vertices_triple``  triple product, BRDF and visibility separate (f3);
+  ``haar_pack_qtree`` converts HAAR1 pyramids to its qtree storage layout
+* ``haar_shift_coeffs_coarse`` coarse-start shift (f4)
 * ``hs_fill_transfer``         seeded synthetic transfer rows generated in place (input generator)
 
 See DESIGN.md for the method, its readings of the paper, layouts and kernels.
@@ -15,6 +19,7 @@ from __future__ import annotations
 
 from ._lib import HaarShiftError, load  # noqa: F401
 from .api import (  # noqa: F401
+    haar_pack_qtree,
     haar_shift_coarse_workspace_bytes,
     haar_shift_coeffs,
     haar_shift_coeffs_coarse,
@@ -28,6 +33,8 @@ from .api import (  # noqa: F401
     relight_sparse_workspace_bytes,
     relight_vertices_shifted,
     relight_vertices_sparse,
+    relight_triple_workspace_bytes,
+    relight_vertices_triple,
     shift_and_relight,
 )
 
@@ -35,5 +42,5 @@ __all__ = [
     "HaarShiftError", "load", "haar_shift_coeffs", "haar_shift_coeffs_coarse", "haar_shift_coarse_workspace_bytes", "haar_shift_workspace_bytes", "hs_fill_transfer",
     "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
     "shift_and_relight", "hs_fill_sparse_transfer", "relight_vertices_sparse",
-    "relight_sparse_workspace_bytes",
+    "relight_sparse_workspace_bytes", "haar_pack_qtree", "relight_triple_workspace_bytes", "relight_vertices_triple",
 ]

@@ -32,6 +32,11 @@ SIGNATURES = {
     "relight_sparse_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int]),
     "hs_fill_sparse_transfer": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_int,
                                            _c.c_int, _c.c_int, _c.c_uint64, _c.c_void_p]),
+    "relight_vertices_triple": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int, _c.c_void_p,
+                                           _c.c_int64, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_size_t, _c.c_void_p]),
+    "relight_triple_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int, _c.c_int, _c.c_int]),
+    "haar_pack_qtree": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int, _c.c_int64, _c.c_int, _c.c_void_p,
+                                   _c.c_void_p]),
     "hs_last_launch_count": (_c.c_int, []),
     "hs_status_string": (_c.c_char_p, [_c.c_int]),
     "hs_last_cuda_error": (_c.c_char_p, []),

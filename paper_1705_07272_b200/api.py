@@ -191,6 +191,61 @@ def relight_vertices_sparse(indices: torch.Tensor, values: torch.Tensor, light: 
     return out
 
 
+def _aligned_workspace(need: int, workspace: Optional[torch.Tensor], device) -> torch.Tensor:
+    if workspace is not None and workspace.numel() * workspace.element_size() >= need and workspace.data_ptr() % 1024 == 0:
+        return workspace
+    ws = torch.empty(need + 1024, dtype=torch.uint8, device=device)
+    return ws[(-ws.data_ptr()) % 1024:]
+
+
+def haar_pack_qtree(coeffs: torch.Tensor, log2k: int, out: Optional[torch.Tensor] = None,
+                    stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """coeffs [rows][faces][stride] (HAAR1, prefix 4**log2k used) -> qtree layout [rows][faces*4**log2k]
+    (include/haarshift.h haar_pack_qtree)."""
+    lib = load()
+    _dev_f32(coeffs, "coeffs")
+    if coeffs.dim() != 3:
+        raise ValueError("coeffs must be [rows][faces][stride]")
+    rows, F, stride = coeffs.shape
+    kf = 4 ** log2k
+    if out is None:
+        out = torch.empty((rows, F * kf), dtype=torch.float32, device=coeffs.device)
+    _dev_f32(out, "out")
+    st = lib.haar_pack_qtree(coeffs.data_ptr(), rows, F, stride, log2k, out.data_ptr(), _stream_ptr(stream))
+    check("haar_pack_qtree", st)
+    return out
+
+
+def relight_triple_workspace_bytes(num_vertices: int, faces: int, k_face: int, batch: int) -> int:
+    return int(load().relight_triple_workspace_bytes(num_vertices, faces, k_face, batch))
+
+
+def relight_vertices_triple(brdf_q: torch.Tensor, vis_q: torch.Tensor, light: torch.Tensor, faces: int, k_face: int,
+                            out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """brdf_q, vis_q [V][faces*k_face] (qtree layout), light [batch][faces][stride >= k_face] (HAAR1)
+    -> radiance [V][batch] = sum_f integral of L * rho * V (triple product, eq:tripleSum)."""
+    lib = load()
+    _dev_f32(brdf_q, "brdf_q")
+    _dev_f32(vis_q, "vis_q")
+    _dev_f32(light, "light")
+    V = brdf_q.shape[0]
+    if brdf_q.numel() != V * faces * k_face or vis_q.shape != brdf_q.shape:
+        raise ValueError("brdf_q and vis_q must be [V][faces*k_face]")
+    if light.dim() != 3 or light.shape[1] != faces:
+        raise ValueError("light must be [batch][faces][stride]")
+    B, _, stride = light.shape
+    if out is None:
+        out = torch.empty((V, B), dtype=torch.float32, device=brdf_q.device)
+    _dev_f32(out, "out")
+    need = relight_triple_workspace_bytes(V, faces, k_face, B)
+    workspace = _aligned_workspace(need, workspace, brdf_q.device)
+    st = lib.relight_vertices_triple(brdf_q.data_ptr(), vis_q.data_ptr(), V, faces, k_face, light.data_ptr(), stride,
+                                     B, out.data_ptr(), workspace.data_ptr(), need, _stream_ptr(stream))
+    check("relight_vertices_triple", st)
+    return out
+
+
 def hs_fill_sparse_transfer(indices: torch.Tensor, values: torch.Tensor, row_start: int, faces: int, log2n: int,
                             dense_levels: int, seed: int, stream: Optional[torch.cuda.Stream] = None):
     """Fill indices/values [rows][K_s] with synth.sparse_transfer_rows (bit for bit)."""

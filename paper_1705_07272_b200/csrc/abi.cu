@@ -254,6 +254,50 @@ hs_status relight_vertices_sparse(const int32_t* indices, const float* values, i
   return s;
 }
 
+hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64_t in_face_stride, int log2k, float* out,
+                          void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!in || !out || rows < 1 || faces < 1 || log2k < 3 || log2k > HS_MAX_LOG2N) return HS_ERR_INVALID_ARG;
+  const long long kf = 1ll << (2 * log2k);
+  if (in_face_stride < kf) return HS_ERR_INVALID_ARG;
+  if (overlap(in, (size_t)((rows * faces - 1) * in_face_stride + kf) * 4, out, (size_t)(rows * faces * kf) * 4))
+    return HS_ERR_INVALID_ARG;
+  if (!aligned16(in) || !aligned16(out)) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_pack_qtree(in, rows, faces, in_face_stride, log2k, out, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
+size_t relight_triple_workspace_bytes(int64_t num_vertices, int faces, int k_face, int batch) {
+  if (num_vertices < 1 || faces < 1 || batch < 1 || batch > 1024 || !is_pow4(k_face) || k_face < 64) return 0;
+  return relight_triple_workspace_bytes_impl(num_vertices, faces, k_face, batch);
+}
+
+hs_status relight_vertices_triple(const float* brdf_q, const float* vis_q, int64_t num_vertices, int faces, int k_face,
+                                  const float* light, int64_t light_face_stride, int batch, float* radiance,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!brdf_q || !vis_q || !light || !radiance || !workspace) return HS_ERR_INVALID_ARG;
+  if (num_vertices < 1 || faces < 1 || batch < 1 || batch > 1024) return HS_ERR_INVALID_ARG;
+  if (!is_pow4(k_face) || k_face < 64 || k_face > (1 << (2 * HS_MAX_LOG2N))) return HS_ERR_INVALID_ARG;
+  if (light_face_stride < k_face || (light_face_stride & 3)) return HS_ERR_INVALID_ARG;
+  if ((long long)faces * k_face > (1ll << 30)) return HS_ERR_INVALID_ARG;
+  if (workspace_bytes < relight_triple_workspace_bytes_impl(num_vertices, faces, k_face, batch)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(brdf_q) || !aligned16(vis_q) || !aligned16(light) || !aligned16(radiance) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 1023))
+    return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_relight_triple(brdf_q, vis_q, num_vertices, faces, k_face, light, light_face_stride, batch, radiance,
+                            workspace, workspace_bytes, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
 hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_t row_start, int64_t row_count, int faces,
                                   int log2n, int k_sparse, int dense_levels, uint64_t seed, void* stream) {
   g_last_launches = 0;

@@ -146,6 +146,13 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
 hs_status launch_relight(const float* T, long long V, int faces, int kface, const float* L,
                          long long lstride, int batch, float* R, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t relight_tc_workspace_bytes(int faces, int kface, int batch);
+// Split-precision light tiles of the tensor-core relight (relight_tc.cu): for frame block fb (64
+// frames) and k block kb (64 columns) a 16 KB pre-swizzled [L_hi | L_lo] tile at
+// ws + (fb * K/64 + kb) * 16 KB, then the per-frame inverse scales (fp32 [batch]).
+constexpr int kTcLTileBytes = 16384;
+hs_status launch_relight_tc_prep(const float* L, long long lstride, int faces, int kface, int batch, void* ws,
+                                 cudaStream_t st);
+bool relight_tc_eligible(int faces, int kface, int batch);
 hs_status launch_rowdot(const float* T, const float* S, long long rows, long long K, float* R,
                         cudaStream_t st);
 bool relight_shifted_fused_supported(int log2n);
@@ -156,6 +163,12 @@ hs_status launch_fill_sparse(int* idx, float* val, long long row_start, long lon
                              int dense_levels, uint64_t seed, cudaStream_t st);
 hs_status launch_relight_sparse(const int* idx, const float* val, long long V, int ks, const float* light, long long C,
                                 int B, float* R, float* Lt, cudaStream_t st);
+hs_status launch_pack_qtree(const float* in, long long rows, int faces, long long in_face_stride, int log2k,
+                            float* out, cudaStream_t st);
+size_t relight_triple_workspace_bytes_impl(long long V, int faces, int kface, int batch);
+hs_status launch_relight_triple(const float* brdf_q, const float* vis_q, long long V, int faces, int kface,
+                                const float* light, long long lstride, int batch, float* R, void* ws, size_t ws_bytes,
+                                cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
                                int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
 

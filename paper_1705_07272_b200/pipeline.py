@@ -56,6 +56,10 @@ class ShiftRelightPipeline:
         self.i = 0
         self.launches = 0
 
+    def _relight_chunk(self, s: int, n: int) -> None:
+        api.relight_vertices(self.T[s:s + n], self.shifted, self.faces, self.k_face, out=self.R[s:s + n],
+                             workspace=self.rws, stream=self.compute)
+
     def step(self, light_host: torch.Tensor, shifts, radiance_host: torch.Tensor) -> torch.cuda.Event:
         """Enqueue one step; returns an event that completes when radiance_host holds the result."""
         buf = self.i & 1
@@ -72,8 +76,7 @@ class ShiftRelightPipeline:
         for c, (s, n) in enumerate(self.chunks):
             if self.i >= 1:
                 self.compute.wait_event(self.ev_copied[c])  # previous step's D2H of this chunk is done
-            api.relight_vertices(self.T[s:s + n], self.shifted, self.faces, self.k_face, out=self.R[s:s + n],
-                                 workspace=self.rws, stream=self.compute)
+            self._relight_chunk(s, n)
             self.launches += api.last_launch_count()
             self.ev_chunk[c].record(self.compute)
             self.d2h.wait_event(self.ev_chunk[c])
@@ -82,3 +85,21 @@ class ShiftRelightPipeline:
                 self.ev_copied[c].record(self.d2h)
         self.i += 1
         return self.ev_copied[-1]
+
+
+class ShiftTripleRelightPipeline(ShiftRelightPipeline):
+    """The same host pipeline with the triple-product relight (row f3): per-vertex BRDF and
+    visibility in the qtree layout (``relight_vertices_triple``) instead of one transfer matrix."""
+
+    def __init__(self, brdf_q: torch.Tensor, vis_q: torch.Tensor, faces: int, log2n: int, batch: int,
+                 band_levels: int, chunks: int = 8, full_pyramids: bool = False):
+        super().__init__(brdf_q, faces, log2n, batch, band_levels, chunks, full_pyramids)
+        self.vis = vis_q
+        rows = max(n for _, n in self.chunks)
+        need = api.relight_triple_workspace_bytes(rows, faces, self.k_face, batch)
+        raw = torch.empty(need + 1024, dtype=torch.uint8, device=brdf_q.device)
+        self.tws = raw[(-raw.data_ptr()) % 1024:]
+
+    def _relight_chunk(self, s: int, n: int) -> None:
+        api.relight_vertices_triple(self.T[s:s + n], self.vis[s:s + n], self.shifted, self.faces, self.k_face,
+                                    out=self.R[s:s + n], workspace=self.tws, stream=self.compute)

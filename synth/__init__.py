@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = [
-    "SEED_BASE", "STREAM_T", "splitmix64", "hash_u64", "hash_uniform", "level_of_index_2d",
+    "SEED_BASE", "STREAM_T", "shading_rows", "STREAM_BRDF", "STREAM_VIS", "splitmix64", "hash_u64", "hash_uniform", "level_of_index_2d",
     "level_of_index_1d", "transfer_rows", "light_pyramids", "random_signals", "CONFIGS",
     "Config", "config", "c1_shifts_1d", "c1_shifts_2d", "c3_shifts", "c4_vertex_shifts",
     "c5_shifts",
@@ -36,6 +36,8 @@ __all__ = [
 
 SEED_BASE = 1705072720          # base seed 1705072720 + config index
 STREAM_T = 0x7A11               # counter-hash stream id of the transfer matrix
+STREAM_BRDF = 0xB2DF            # triple product (row f3): per-vertex BRDF rows (transfer_rows layout)
+STREAM_VIS = 0x7151             # triple product (row f3): per-vertex visibility rows
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 _GOLD = np.uint64(0x9E3779B97F4A7C15)
@@ -84,7 +86,8 @@ def level_of_index_1d(k: np.ndarray) -> np.ndarray:
     return _floor_log2(np.asarray(k, dtype=np.int64))
 
 
-def transfer_rows(seed: int, row_start: int, row_count: int, faces: int, k_face: int) -> np.ndarray:
+def transfer_rows(seed: int, row_start: int, row_count: int, faces: int, k_face: int,
+                  stream: int = STREAM_T) -> np.ndarray:
     """Rows [row_start, row_start+row_count) of the transfer matrix T, fp32 [rows][faces*k_face].
 
     T[v][f*k_face + k] = u * 2**-level(k), u = hash_uniform(seed, STREAM_T, v*faces*k_face +
@@ -95,13 +98,25 @@ def transfer_rows(seed: int, row_start: int, row_count: int, faces: int, k_face:
     kt = faces * k_face
     v = np.arange(row_start, row_start + row_count, dtype=np.uint64)[:, None]
     col = np.arange(kt, dtype=np.uint64)[None, :]
-    u = hash_uniform(seed, STREAM_T, v * np.uint64(kt) + col)
+    u = hash_uniform(seed, stream, v * np.uint64(kt) + col)
     k = (np.arange(kt) % k_face)
     lev = level_of_index_2d(k)
     scale = np.ldexp(np.float32(1.0), -lev).astype(np.float32)
     t = u * scale[None, :]
     t[:, k == 0] = np.abs(t[:, k == 0])
     return t.astype(np.float32)
+
+
+def shading_rows(seed: int, row_start: int, row_count: int, faces: int, k_face: int, stream: int) -> np.ndarray:
+    """Per-vertex BRDF or visibility rows for the triple product (row f3), fp32 [rows][faces*k_face]:
+    transfer_rows(stream) with the details scaled by 1/4 and the scaling entry mapped to
+    0.5 + 0.5 |u| -- functions with a positive mean in [0.5, 1) and detail contrast, like a BRDF lobe
+    or a visibility mask.  The device side reproduces it bit for bit with
+    hs_fill_transfer followed by the same two fp32 operations (bench.py fill_shading)."""
+    t = transfer_rows(seed, row_start, row_count, faces, k_face, stream)
+    out = (t * np.float32(0.25)).astype(np.float32)
+    out[:, ::k_face] = np.float32(0.5) + t[:, ::k_face] * np.float32(0.5)
+    return out
 
 
 STREAM_TS = 0x5A12              # counter-hash stream of the sparse transfer
@@ -282,6 +297,8 @@ CONFIGS = {
     "c5s": Config("c5s", 8, 6, 1000000, 8, 64, SEED_BASE + 5,
                   "c5 with sparse top-K transfer (K_s = 256 full-resolution coefficients per vertex, row f2)",
                   {"k_sparse": 256, "dense_levels": 2}),
+    "c5t": Config("c5t", 8, 6, 1000000, 5, 64, SEED_BASE + 5,
+                  "c5 with the triple product (row f3): per-vertex BRDF and visibility, each 6 x 1024 coefficients"),
 }
 
 
