@@ -112,7 +112,6 @@ struct ShiftArgs {
   const float* in;            // face g reads in + (g / faces) * in_batch_stride + (g % faces) * K
   float* out;                 // face g writes out + g * out_face_stride
   float* ws;                  // per-face coarse fields (see shift_workspace_layout)
-  unsigned* counters;         // per-face tile-completion counters (zeroed before launch)
   const FaceParam* dev_fp;    // device FaceParams (per-vertex path) or nullptr -> use fp[]
   long long in_batch_stride;  // elements; 0 broadcasts one pyramid set to every batch entry
   long long in_face_stride;   // elements between the faces of one batch entry (>= K)
@@ -128,12 +127,11 @@ constexpr int kTileTC = 8;    // tile side at level c (cells)
 inline int coarse_level(int m) { return m > kTileKF ? m - kTileKF : 0; }
 bool shift2d_uses_fp64(int log2n);        // field precision of the 2D tile kernel
 inline long long ws_face_floats_2d(int n) {  // elements of the field type per face
+  // [shifted level-c fields 3*4^c][unshifted level-c fields 3*4^c][scratch 3*4^(c-1)]
   int c = coarse_level(n);
-  long long a = 3ll << (2 * c);
-  long long b = c > 0 ? (3ll << (2 * (c - 1))) : 0;
-  return a + b;
+  if (c == 0) return 0;
+  return 6ll * (1ll << (2 * c)) + 3ll * (1ll << (2 * (c - 1)));
 }
-
 size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces);
 hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int faces,
                        long long num_faces, long long in_batch_stride, long long in_face_stride,

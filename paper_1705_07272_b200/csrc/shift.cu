@@ -10,7 +10,7 @@
 
 namespace hs {
 
-hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_perm, cudaStream_t st);
+hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, cudaStream_t st);
 int shift2d_tiles_for(int m);
 
 namespace {
@@ -101,14 +101,12 @@ __global__ void face_params_kernel(const float* __restrict__ shifts, long long n
   for (int f = 0; f < faces; ++f) fp[v * faces + f] = p;
 }
 
-inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-
 }  // namespace
 
 size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces) {
   if (ndim != 2) return 0;
   const size_t esz = shift2d_uses_fp64(log2n) ? 8 : 4;
-  return align256((size_t)num_faces * sizeof(unsigned)) + (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * esz;
+  return (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * esz;
 }
 
 // in:  [num_faces / faces batches][faces][K]; out [num_faces][Kb]
@@ -120,16 +118,9 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
   const int n = log2n;
   const long long K = (ndim == 2) ? (1ll << (2 * n)) : (1ll << n);
   const long long Kb = (ndim == 2) ? (1ll << (2 * band)) : (1ll << band);
-  unsigned* counters = nullptr;
   float* wsf = nullptr;
   const long long wsface = (ndim == 2) ? ws_face_floats_2d(n) : 0;
-  if (ndim == 2) {
-    counters = reinterpret_cast<unsigned*>(ws);
-    wsf = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
-                                   align256((size_t)num_faces * sizeof(unsigned)));
-    HS_CHECK_CUDA(cudaMemsetAsync(counters, 0, (size_t)num_faces * sizeof(unsigned), st),
-                  "cudaMemsetAsync(counters)");  // a memset, not one of our kernels: not counted
-  }
+  if (ndim == 2) wsf = reinterpret_cast<float*>(ws);
   const long long batches = num_faces / faces;
   const long long chunk_b = std::max<long long>(1, kMaxFacesPerLaunch / faces);
   ShiftArgs a;
@@ -142,7 +133,6 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     a.ws = wsf ? reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) +
                                          g0 * wsface * (shift2d_uses_fp64(n) ? 8 : 4))
                : nullptr;
-    a.counters = counters ? counters + g0 : nullptr;
     a.dev_fp = nullptr;
     a.in_batch_stride = in_batch_stride;
     a.in_face_stride = in_face_stride;
@@ -153,13 +143,14 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     a.out_face_stride = (int)Kb;
     a.num_faces = nf;
     int max_tiles = 0;
-    bool any_perm = false;
+    bool any_perm = false, any_coarse = false;
     if (shifts_host) {
       for (int i = 0; i < nf; ++i) {
         const double* s = shifts_host + (g0 + i) * ndim;
         a.fp[i] = (ndim == 2) ? make_face_param_2d(s[0], s[1], n) : make_face_param_1d(s[0], n);
         max_tiles = std::max(max_tiles, shift2d_tiles_for(a.fp[i].m));
         if (a.fp[i].m < band || a.fp[i].m == 0) any_perm = true;
+        if (coarse_level(a.fp[i].m) > 0) any_coarse = true;
       }
     } else {
       // per-vertex device shifts: FaceParams computed on the device (one per vertex and face)
@@ -171,9 +162,10 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
       a.dev_fp = dfp;
       max_tiles = shift2d_tiles_for(n);
       any_perm = true;
+      any_coarse = coarse_level(n) > 0;
     }
     if (ndim == 2) {
-      hs_status s = launch_shift2d(a, max_tiles, any_perm, st);
+      hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, st);
       if (s != HS_OK) return s;
     } else {
       const size_t smem = (size_t)2 * (1u << n) * sizeof(float);

@@ -24,13 +24,16 @@
 //        Z'_l = 1/4 [1,2,1] (x) [1,2,1] Z'_{l+1} |v2,     D^'_l = Z'_{l+1}[2i][2j] / 4
 //      Steps (2) and the first step of (3) are fused into one separable stencil on F_m.
 //
-// Tiling: a CTA owns a TC x TC tile at the tile-root level c = max(0, m - KF) and every output
-// coefficient below it at levels c..m-1.  All detail windows it needs (its ancestors' few cells
-// at levels < c plus tile + halo at levels c..m-1) are fetched up front with cp.async (one
-// latency round trip); it then recomputes the ancestors' fields top-down from level 0, runs
-// (1)-(3) over its window (all periodic index arithmetic on unwrapped coordinates), writes its
-// outputs and its shifted level-c fields.  The last CTA of a face to finish (atomic ticket) runs
-// the coarse bottom-up c -> 0.  Levels >= m (dyadic shifts) are exact permutations.
+// Three launches per call:
+//   coarse_fields_kernel  one CTA per face: (1) top-down over the full grid to the tile-root level
+//                         c = max(0, m - KF) -> the unshifted level-c fields (workspace);
+//   shift2d_tile_kernel   a CTA owns a TC x TC tile at level c and every output coefficient below
+//                         it at levels c..m-1: it fetches its window of the level-c fields and the
+//                         detail windows of levels c..m-1 with cp.async (one latency round trip),
+//                         runs (1)-(3) over its window (all periodic index arithmetic on unwrapped
+//                         coordinates), writes its outputs and its shifted level-c fields;
+//   coarse_finish_kernel  one CTA per face: the coarse bottom-up c -> 0 from the shifted fields.
+// Levels >= m (dyadic shifts) are exact permutations (permute_kernel).
 //
 // Field precision FT: fp32 for log2n <= 8; fp64 above (DESIGN.md §4.1 error model: fine-level
 // fp32 rounding is amplified ~2^(n-l) on the coarse outputs of large faces).
@@ -63,6 +66,15 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                "l"(src)
                : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+template <typename FT>
+__device__ __forceinline__ void cp_async_ft(FT* dst, const FT* src) {
+  if constexpr (sizeof(FT) == 8) cp_async8(dst, src); else cp_async4(dst, src);
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -213,8 +225,8 @@ __device__ __forceinline__ void load_window_vec(const float* __restrict__ in, fl
 
 template <typename FT, int K, int TC>
 __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* smem, const FaceParam& P, int g,
-                                          int m, int c, int i0, int j0, int tpr, int (*sR)[2][HS_MAX_LOG2N + 1],
-                                          int* sDoff, int* sLast) {
+                                          int m, int c, int i0, int j0, int (*sR)[2][HS_MAX_LOG2N + 1],
+                                          int* sDoff) {
   using G = TGeo<K, TC>;
   using S = TSmem<FT, K, TC>;
   constexpr int CB = G::CB, HC = G::HC, CHR = G::CHR, SN1 = G::SN1;
@@ -259,7 +271,19 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   //      group B = the large windows of levels m-2 and m-1; the ancestors' top-down runs while
   //      group B is still in flight.  Per level d = m - l the window side is a compile-time
   //      constant, so the element decode uses constant divisors.
-  load_windows<G, 3, HS_MAX_LOG2N>(in, sDet, sR, sDoff, m);  // group A: d = 3 .. m
+  load_windows<G, 3, K>(in, sDet, sR, sDoff, m);             // group A: d = 3 .. K (levels c .. m-3)
+  if (c > 0) {                                                 // group A: unshifted level-c fields
+    const int gc = 1 << c, cm = gc - 1;
+    const int pw = sR[0][1][c], ys = sR[0][0][c], xs = sR[1][0][c];
+    const FT* src = reinterpret_cast<const FT*>(args.ws) + (long long)g * args.ws_face_stride + 3ll * gc * gc;
+    FT* dst = sCh + ((((K - 2) & 1) == 0) ? 3 * G::ANC_MAX * G::ANC_MAX : 0);
+    for (int e = tid; e < 3 * pw * pw; e += kThreads) {
+      const int t = e / (pw * pw), rem = e - t * pw * pw;
+      const int a = rem / pw, bb = rem - a * pw;
+      cp_async_ft<FT>(dst + t * G::ANC_MAX * G::ANC_MAX + a * pw + bb,
+                      src + (long long)t * gc * gc + (long long)((ys + a) & cm) * gc + ((xs + bb) & cm));
+    }
+  }
   cp_async_commit();
   if (m - 1 >= 2)
     load_window_vec<G>(in, sDet, sR, sDoff, m);               // group B: d = 1 (16-byte chunks)
@@ -286,7 +310,9 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     const FT* pf = sCh + ((((m - 2 - l) & 1) == 0) ? 3 * G::ANC_MAX * G::ANC_MAX : 0);
     const int pplane = G::ANC_MAX * G::ANC_MAX;
     int pstride = 0, poy = 0, pox = 0;
-    if (l > 0) {
+    if (l == c) {
+      pstride = pw;                 // the level-c window loaded from coarse_fields_kernel
+    } else if (l > 0) {
       pstride = 2 * sR[0][1][l - 1];
       poy = ys - 2 * sR[0][0][l - 1];
       pox = xs - 2 * sR[1][0][l - 1];
@@ -333,7 +359,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     __syncthreads();
   };
   HS_PHASE(3)
-  for (int l = 0; l + 2 < m; ++l) ancestor_level(l);  // uses group A only
+  for (int l = c; l + 2 < m; ++l) ancestor_level(l);  // uses group A only
   cp_async_wait_all();
   __syncthreads();
   HS_PHASE(4)
@@ -518,7 +544,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   if (blockIdx.x == 0 && tid == 0) out[0] = __ldg(in);  // scaling coefficient: unchanged (R8)
   if (c == 0) return;
 
-  // ---- publish the owned level-c fields; the last tile of the face runs the coarse finish
+  // ---- publish the owned shifted level-c fields (coarse_finish_kernel runs the bottom-up c -> 0)
   const int gc = 1 << c;
   FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
   for (int idx = tid; idx < 3 * TC * TC; idx += kThreads) {
@@ -526,24 +552,100 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     const int ii = r / TC, jj = r - ii * TC;
     wsf[(long long)fld * gc * gc + (long long)(i0 + ii) * gc + (j0 + jj)] = srcS[fld * srcPlane + ii * srcN + jj];
   }
-  __syncthreads();  // all of this CTA's field writes happen-before thread 0's release below
-  if (tid == 0) {
-    unsigned prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(args.counters + g) : "memory");
-    *sLast = (prev == (unsigned)(tpr * tpr - 1));
+}
+
+// (1) over the full grid of one face up to the tile-root level c: the unshifted level-c fields,
+// ping-ponging the intermediate levels through the (not yet used) shifted-field and scratch areas.
+template <typename FT>
+__global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_constant__ ShiftArgs args) {
+  const int g = blockIdx.x;
+  const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
+  const int c = P.m > KF ? P.m - KF : 0;
+  if (c == 0) return;
+  const int b = g / args.faces, f = g % args.faces;
+  const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
+  FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
+  const long long GC = 1ll << (2 * c);
+  FT* const bufA = wsf;                 // shifted-field area (3 * 4^c)
+  FT* const bufB = wsf + 6 * GC;        // scratch (3 * 4^(c-1))
+  FT* const fin = wsf + 3 * GC;         // unshifted level-c fields
+  for (int l = 0; l < c; ++l) {
+    const int gl = 1 << l, G2 = 2 * gl;
+    const FT asc = FT(pow2f(l));
+    const FT* cur = ((c - l) & 1) ? bufB : bufA;       // level l fields (l > 0)
+    FT* nxt = (l + 1 == c) ? fin : (((c - l - 1) & 1) ? bufB : bufA);
+    for (int idx = threadIdx.x; idx < gl * gl; idx += blockDim.x) {
+      const int i = idx >> l, j = idx & (gl - 1);
+      FT d[2][2][2][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const long long o = (long long)((i + u) & (gl - 1)) * gl + ((j + v) & (gl - 1));
+          const FT H = FT(__ldg(in + (long long)gl * gl * 1 + o)) * asc;
+          const FT V = FT(__ldg(in + (long long)gl * gl * 2 + o)) * asc;
+          const FT D = FT(__ldg(in + (long long)gl * gl * 3 + o)) * asc;
+          d[u][v][0][0] = H + V + D;
+          d[u][v][0][1] = -H + V - D;
+          d[u][v][1][0] = H - V - D;
+          d[u][v][1][1] = -H - V + D;
+        }
+      FT Xl = FT(0), Yl = FT(0), Zl = FT(0);
+      if (l > 0) {
+        Xl = __ldcg(cur + idx);
+        Yl = __ldcg(cur + gl * gl + idx);
+        Zl = __ldcg(cur + 2 * gl * gl + idx);
+      }
+      FT cx[2][2], cy[2][2], cz[2][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        cx[a][0] = d[0][0][a][0] - d[0][0][a][1];
+        cx[a][1] = Xl + d[0][0][a][1] - d[0][1][a][0];
+      }
+#pragma unroll
+      for (int bq = 0; bq < 2; ++bq) {
+        cy[0][bq] = d[0][0][0][bq] - d[0][0][1][bq];
+        cy[1][bq] = Yl + d[0][0][1][bq] - d[1][0][0][bq];
+      }
+      cz[0][0] = d[0][0][0][0] - d[0][0][0][1] - d[0][0][1][0] + d[0][0][1][1];
+      cz[0][1] = d[0][0][0][1] - d[0][0][1][1] - d[0][1][0][0] + d[0][1][1][0];
+      cz[1][0] = d[0][0][1][0] - d[0][0][1][1] - d[1][0][0][0] + d[1][0][0][1];
+      cz[1][1] = Zl + d[0][0][1][1] - d[0][1][1][0] - d[1][0][0][1] + d[1][1][0][0];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bq = 0; bq < 2; ++bq) {
+          const long long o = (long long)(2 * i + a) * G2 + (2 * j + bq);
+          nxt[o] = cx[a][bq];
+          nxt[(long long)G2 * G2 + o] = cy[a][bq];
+          nxt[2ll * G2 * G2 + o] = cz[a][bq];
+        }
+    }
+    __syncthreads();
   }
-  __syncthreads();  // thread 0's acquire (other tiles' fields visible) orders the reads below
-  HS_PHASE(9)
-  if (!*sLast) return;
+}
+
+// The coarse bottom-up c -> 0 of one face from the tiles' shifted level-c fields.
+constexpr int kFinishSmem = 64 * 1024;
+template <typename FT>
+__global__ void __launch_bounds__(kThreads) coarse_finish_kernel(const __grid_constant__ ShiftArgs args) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int g = blockIdx.x;
+  const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
+  const int c = P.m > KF ? P.m - KF : 0;
+  if (c == 0) return;
+  float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
+  FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
+  const int gc = 1 << c;
   const long long need = 3ll * gc * gc + 3ll * (gc / 2) * (gc / 2);
-  if (need * (long long)sizeof(FT) <= (long long)S::BYTES) {
+  if (need * (long long)sizeof(FT) <= (long long)kFinishSmem) {
     FT* A = reinterpret_cast<FT*>(smem);
     FT* B0 = A + 3 * gc * gc;
-    for (int idx = tid; idx < 3 * gc * gc; idx += kThreads) A[idx] = __ldcg(wsf + idx);
+    for (int idx = threadIdx.x; idx < 3 * gc * gc; idx += kThreads) A[idx] = __ldcg(wsf + idx);
     __syncthreads();
-    coarse_finish<FT>(A, B0, A, c, out, band, false);
+    coarse_finish<FT>(A, B0, A, c, out, args.band, false);
   } else {
-    coarse_finish<FT>(wsf, wsf + 3ll * gc * gc, wsf, c, out, band, true);
+    coarse_finish<FT>(wsf, wsf + 6ll * gc * gc, wsf, c, out, args.band, true);
   }
 }
 
@@ -558,7 +660,6 @@ __global__ void __launch_bounds__(kThreads, 2) shift2d_tile_kernel(const __grid_
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int sR[2][2][HS_MAX_LOG2N + 1];
   __shared__ int sDoff[HS_MAX_LOG2N + 2];
-  __shared__ int sLast;
   const int g = blockIdx.y;  // face within this launch
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int m = P.m;
@@ -572,15 +673,15 @@ __global__ void __launch_bounds__(kThreads, 2) shift2d_tile_kernel(const __grid_
   const int j0 = (blockIdx.x % tpr) * tc;
   if (k == 3) {
     switch (tc) {
-      case 8: tile_body<FT, 3, 8>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
-      case 4: tile_body<FT, 3, 4>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
-      case 2: tile_body<FT, 3, 2>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
-      default: tile_body<FT, 3, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast); break;
+      case 8: tile_body<FT, 3, 8>(args, smem, P, g, m, c, i0, j0, sR, sDoff); break;
+      case 4: tile_body<FT, 3, 4>(args, smem, P, g, m, c, i0, j0, sR, sDoff); break;
+      case 2: tile_body<FT, 3, 2>(args, smem, P, g, m, c, i0, j0, sR, sDoff); break;
+      default: tile_body<FT, 3, 1>(args, smem, P, g, m, c, i0, j0, sR, sDoff); break;
     }
   } else if (k == 2) {
-    tile_body<FT, 2, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast);
+    tile_body<FT, 2, 1>(args, smem, P, g, m, c, i0, j0, sR, sDoff);
   } else {
-    tile_body<FT, 1, 1>(args, smem, P, g, m, c, i0, j0, tpr, sR, sDoff, &sLast);
+    tile_body<FT, 1, 1>(args, smem, P, g, m, c, i0, j0, sR, sDoff);
   }
 }
 
@@ -618,16 +719,27 @@ __global__ void permute_kernel(const __grid_constant__ ShiftArgs args) {
 }
 
 template <typename FT>
-hs_status launch_tiles(ShiftArgs& a, int max_tiles, cudaStream_t st) {
+hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_t st) {
   static bool attr_done = false;  // idempotent attribute set (benign race: same value)
   if (!attr_done) {
     HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_tile_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_tile_smem<FT>()),
                   "cudaFuncSetAttribute(shift2d_tile_kernel)");
+    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_finish_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFinishSmem),
+                  "cudaFuncSetAttribute(coarse_finish_kernel)");
     attr_done = true;
+  }
+  if (any_coarse) {
+    coarse_fields_kernel<FT><<<a.num_faces, kThreads, 0, st>>>(a);
+    HS_CHECK_LAUNCH("coarse_fields_kernel");
   }
   shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);
   HS_CHECK_LAUNCH("shift2d_tile_kernel");
+  if (any_coarse) {
+    coarse_finish_kernel<FT><<<a.num_faces, kThreads, kFinishSmem, st>>>(a);
+    HS_CHECK_LAUNCH("coarse_finish_kernel");
+  }
   return HS_OK;
 }
 
@@ -635,10 +747,10 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, cudaStream_t st) {
 
 bool shift2d_uses_fp64(int log2n) { return log2n >= 9; }
 
-hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_perm, cudaStream_t st) {
+hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, cudaStream_t st) {
   if (max_tiles > 0) {
-    hs_status s = shift2d_uses_fp64(a.log2n) ? launch_tiles<double>(a, max_tiles, st)
-                                             : launch_tiles<float>(a, max_tiles, st);
+    hs_status s = shift2d_uses_fp64(a.log2n) ? launch_tiles<double>(a, max_tiles, any_coarse, st)
+                                             : launch_tiles<float>(a, max_tiles, any_coarse, st);
     if (s != HS_OK) return s;
   }
   if (any_perm) {

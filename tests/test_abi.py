@@ -48,8 +48,9 @@ def test_status_strings_and_version(lib):
 def test_workspace_sizes(lib):
     assert lib.haar_shift_workspace_bytes(1, 3, 1, 1) == 0
     w = lib.haar_shift_workspace_bytes(2, 8, 6, 64)
-    # counters (aligned 256) + per face 3*4^5 + 3*4^4 floats
-    assert w == ((384 * 4 + 255) // 256) * 256 + 384 * (3 * 1024 + 3 * 256) * 4
+    # per face: shifted + unshifted level-5 fields (2 * 3*4^5) + scratch 3*4^4 floats
+    assert w == 384 * (6 * 1024 + 3 * 256) * 4
+    assert lib.haar_shift_workspace_bytes(2, 3, 6, 64) == 0                                        # c = 0
     assert lib.haar_shift_workspace_bytes(2, 0, 1, 1) == 0
     assert lib.haar_shift_workspace_bytes(2, 13, 1, 1) == 0
     assert lib.relight_shifted_workspace_bytes(100000, 6, 7) >= 3 * 6 * 16384 * 4 + 100000 * 18 * 4  # fused: fields + partials
@@ -76,7 +77,7 @@ def test_shift_validation_before_device(lib):
     assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 4, FAKE * 8, 1 << 20, None) == 1         # band > log2n
     assert f(FAKE, FAKE, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1             # in == out
     assert f(FAKE, FAKE + 64, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1        # overlap
-    assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, None, 0, None) == 1                   # no workspace
+    assert f(FAKE, FAKE * 4, 2, 4, 1, 1, p, 4, None, 0, None) == 1                   # no workspace (log2n 4)
     a[1] = np.nan
     assert f(FAKE, FAKE * 4, 2, 3, 1, 1, p, 3, FAKE * 8, 1 << 20, None) == 1         # non-finite shift
     a[1] = np.inf
