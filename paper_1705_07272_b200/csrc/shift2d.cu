@@ -168,9 +168,11 @@ struct TSmem {
   using G = TGeo<K, TC>;
   static constexpr int DET = 0;                                                      // float
   static constexpr int B1 = (DET + G::DET_MAX * 4 + 15) / 16 * 16;                   // FT[3][CB^2]
-  static constexpr int CHILD = B1 + 3 * G::CB * G::CB * (int)sizeof(FT);             // FT[3][2][CHR][HC]
-  static constexpr int BYTES = CHILD + 3 * 2 * G::CHR * G::HC * (int)sizeof(FT);
-  static_assert(3 * G::ANC_MAX * G::ANC_MAX <= 3 * 2 * G::CHR * G::HC, "ancestor fields alias the child planes");
+  static constexpr int CHILD = B1 + 3 * G::CB * G::CB * (int)sizeof(FT);             // FT[2][CHR][HC], one field
+  // the child plane also holds the two ancestor-field halves (3 ANC_MAX^2 each) before step (1')
+  static constexpr int CHILD_ELEMS = (2 * G::CHR * G::HC > 6 * G::ANC_MAX * G::ANC_MAX) ? 2 * G::CHR * G::HC
+                                                                                       : 6 * G::ANC_MAX * G::ANC_MAX;
+  static constexpr int BYTES = CHILD + CHILD_ELEMS * (int)sizeof(FT);
   static_assert(3 * G::SN1 * G::SN1 <= 3 * G::CB * G::CB, "shifted m-1 window aliases B1");
 };
 
@@ -366,7 +368,10 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   if (m >= 2) ancestor_level(m - 2);                  // level m-1 fields (group B)
 
   HS_PHASE(5)
-  // ---- (1') level m-1 -> m, all three fields per parent, parity-split child planes
+  // ---- per field t in {X, Y, Z}: (1') its level-m children (one parity-split plane, so three
+  //      fields never share memory) then (2)+(3) the fused shift + first bottom-up stencil with a
+  //      register-sliding window down each thread's strip; shifted level-(m-1) field t -> sB1
+  //      plane t (whose unshifted content only field t's children needed), outputs -> global
   {
     const int l = m - 1;
     const int ys = sR[0][0][l], xs = sR[1][0][l];
@@ -382,56 +387,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
       pox = xs - 2 * sR[1][0][l - 1];
     }
     constexpr int NP = G::P1 * G::P1;
-#pragma unroll 1
-    for (int idx = tid; idx < NP; idx += kThreads) {
-      const int pi = idx / G::P1, pj = idx - pi * G::P1;  // constant divisor
-      const int o = pi * RW + pj;
-      FT H[4], V[4], D[4];  // cells (i,j), (i,j+1), (i+1,j), (i+1,j+1)
-      const int oo[4] = {o, o + 1, o + RW, o + RW + 1};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        H[q] = FT(dt[oo[q]]) * asc;
-        V[q] = FT(dt[DPL + oo[q]]) * asc;
-        D[q] = FT(dt[2 * DPL + oo[q]]) * asc;
-      }
-      const FT d00 = H[0] + V[0] + D[0], d01 = -H[0] + V[0] - D[0], d10 = H[0] - V[0] - D[0],
-               d11 = -H[0] - V[0] + D[0];
-      const FT r00 = H[1] + V[1] + D[1], r10 = H[1] - V[1] - D[1];
-      const FT b00 = H[2] + V[2] + D[2], b01 = -H[2] + V[2] - D[2];
-      const FT g00 = H[3] + V[3] + D[3];
-      FT Xl = FT(0), Yl = FT(0), Zl = FT(0);
-      if (l > 0) {
-        const int po = (pi + poy) * CB + (pj + pox);
-        Xl = sB1[po];
-        Yl = sB1[CB * CB + po];
-        Zl = sB1[2 * CB * CB + po];
-      }
-      FT* c0 = sCh + (2 * pi) * HC + pj;  // field 0, even plane, row 2pi
-      // X
-      c0[0] = d00 - d01;
-      c0[PLANE_C] = Xl + d01 - r00;
-      c0[HC] = d10 - d11;
-      c0[PLANE_C + HC] = Xl + d11 - r10;
-      // Y
-      FT* c1 = c0 + 2 * PLANE_C;
-      c1[0] = d00 - d10;
-      c1[PLANE_C] = d01 - d11;
-      c1[HC] = Yl + d10 - b00;
-      c1[PLANE_C + HC] = Yl + d11 - b01;
-      // Z
-      FT* c2 = c0 + 4 * PLANE_C;
-      c2[0] = FT(4) * D[0];
-      c2[PLANE_C] = d01 - d11 - r00 + r10;
-      c2[HC] = d10 - d11 - b00 + b01;
-      c2[PLANE_C + HC] = Zl + d11 - r10 - b01 + g00;
-    }
-    __syncthreads();
-  }
 
-  HS_PHASE(6)
-  // ---- (2)+(3) fused shift + first bottom-up: register-sliding window down each thread's strip,
-  //      taps at immediate offsets; shifted level-(m-1) fields -> sB1, owned outputs -> global
-  {
     const int k1 = K - 1;
     const int Ssy = i0 << k1, Ssx = j0 << k1;
     constexpr int ON1 = TC << (K - 1);
@@ -441,23 +397,65 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     const FT ta = wx1, tb0 = wx0 + FT(2) * wx1, tb1 = FT(2) * wx0 + wx1, tcc = wx0;
     const FT ua = wy1, ub0 = wy0 + FT(2) * wy1, ub1 = FT(2) * wy0 + wy1, uc = wy0;
     const FT q = FT(0.25);
-    const int lv = m - 1;
-    const int gl = 1 << lv;
-    const FT osc = FT(pow2f(-lv));
-    const bool emit = lv < band;
+    const int gl = 1 << l;
+    const FT osc = FT(pow2f(-l));
+    const bool emit = l < band;
     const int strip = tid / SN1, jj = tid - strip * SN1;
-    if (strip < G::NSTRIP) {
-      const int ii0 = strip * G::RSS;
-      const int rb = 2 * (Ssy + ii0) - P.Qy - Cy - 1;  // window row 0 = tap -1 of row ii0
-      constexpr int NW = 2 * G::RSS + 2;
+
 #pragma unroll
-      for (int fld = 0; fld < 3; ++fld) {
-        const FT* pl = sCh + fld * 2 * PLANE_C;
+    for (int fld = 0; fld < 3; ++fld) {
+      // (1') children of field fld
+#pragma unroll 1
+      for (int idx = tid; idx < NP; idx += kThreads) {
+        const int pi = idx / G::P1, pj = idx - pi * G::P1;  // constant divisor
+        const int o = pi * RW + pj;
+        const FT H0 = FT(dt[o]) * asc, V0 = FT(dt[DPL + o]) * asc, D0 = FT(dt[2 * DPL + o]) * asc;
+        const FT d00 = H0 + V0 + D0, d01 = -H0 + V0 - D0, d10 = H0 - V0 - D0, d11 = -H0 - V0 + D0;
+        FT pf = FT(0);
+        if (l > 0) pf = sB1[fld * CB * CB + (pi + poy) * CB + (pj + pox)];
+        FT* c0 = sCh + (2 * pi) * HC + pj;  // even plane, row 2pi
+        if (fld == 0) {
+          const int o1 = o + 1;
+          const FT H1 = FT(dt[o1]) * asc, V1 = FT(dt[DPL + o1]) * asc, D1 = FT(dt[2 * DPL + o1]) * asc;
+          const FT r00 = H1 + V1 + D1, r10 = H1 - V1 - D1;
+          c0[0] = d00 - d01;
+          c0[PLANE_C] = pf + d01 - r00;
+          c0[HC] = d10 - d11;
+          c0[PLANE_C + HC] = pf + d11 - r10;
+        } else if (fld == 1) {
+          const int o2 = o + RW;
+          const FT H2 = FT(dt[o2]) * asc, V2 = FT(dt[DPL + o2]) * asc, D2 = FT(dt[2 * DPL + o2]) * asc;
+          const FT b00 = H2 + V2 + D2, b01 = -H2 + V2 - D2;
+          c0[0] = d00 - d10;
+          c0[PLANE_C] = d01 - d11;
+          c0[HC] = pf + d10 - b00;
+          c0[PLANE_C + HC] = pf + d11 - b01;
+        } else {
+          const int o1 = o + 1, o2 = o + RW, o3 = o + RW + 1;
+          const FT H1 = FT(dt[o1]) * asc, V1 = FT(dt[DPL + o1]) * asc, D1 = FT(dt[2 * DPL + o1]) * asc;
+          const FT H2 = FT(dt[o2]) * asc, V2 = FT(dt[DPL + o2]) * asc, D2 = FT(dt[2 * DPL + o2]) * asc;
+          const FT H3 = FT(dt[o3]) * asc, V3 = FT(dt[DPL + o3]) * asc, D3 = FT(dt[2 * DPL + o3]) * asc;
+          const FT r00 = H1 + V1 + D1, r10 = H1 - V1 - D1;
+          const FT b00 = H2 + V2 + D2, b01 = -H2 + V2 - D2;
+          const FT g00 = H3 + V3 + D3;
+          c0[0] = FT(4) * D0;
+          c0[PLANE_C] = d01 - d11 - r00 + r10;
+          c0[HC] = d10 - d11 - b00 + b01;
+          c0[PLANE_C + HC] = pf + d11 - r10 - b01 + g00;
+        }
+      }
+      __syncthreads();
+
+      // (2)+(3) fused stencil of field fld
+      if (strip < G::NSTRIP) {
+        const int ii0 = strip * G::RSS;
+        const int rb = 2 * (Ssy + ii0) - P.Qy - Cy - 1;  // window row 0 = tap -1 of row ii0
+        constexpr int NW = 2 * G::RSS + 2;
         const FT* base[4];
 #pragma unroll
         for (int vv = 0; vv < 4; ++vv) {
           const int cl = 2 * (Ssx + jj) - P.Qx - Cx + vv - 1;
-          base[vv] = pl + (cl & 1) * PLANE_C + rb * HC + (cl >> 1);
+          base[vv] = sCh + (cl & 1) * PLANE_C + rb * HC + (cl >> 1);
         }
         FT hA[NW], hB[NW];
 #pragma unroll
@@ -472,8 +470,9 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
             hB[w] = wx1 * x_1 + wx0 * x0;
           }
         }
-        FT* dstS = sB1 + fld * CB * CB;
-        float* ob = out + (long long)gl * gl * (1 + fld);
+        FT* dstS = sB1 + fld * CB * CB + ii0 * SN1 + jj;
+        float* ob = out + (long long)gl * gl * (1 + fld) + (Ssy + ii0) * gl + (Ssx + jj);
+        const bool emit_col = emit && jj < ON1;
 #pragma unroll
         for (int r = 0; r < G::RSS; ++r) {
           const int ii = ii0 + r;
@@ -487,13 +486,13 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
               fv = q * (ua * hA[u] + ub0 * hA[u + 1] + ub1 * hA[u + 2] + uc * hA[u + 3]);
               dv = q * (wy1 * hB[u] + wy0 * hB[u + 1]);
             }
-            dstS[ii * SN1 + jj] = fv;
-            if (ii < ON1 && jj < ON1 && emit) ob[(Ssy + ii) * gl + (Ssx + jj)] = (float)(dv * osc);
+            dstS[r * SN1] = fv;
+            if (emit_col && ii < ON1) ob[r * gl] = (float)(dv * osc);
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
 
   HS_PHASE(7)
@@ -554,10 +553,13 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   }
 }
 
-// (1) over the full grid of one face up to the tile-root level c: the unshifted level-c fields,
-// ping-ponging the intermediate levels through the (not yet used) shifted-field and scratch areas.
+// (1) over the full grid of one face up to the tile-root level c: the unshifted level-c fields.
+// Intermediate levels ping-pong in shared memory when they fit (else through the not yet used
+// shifted-field and scratch areas of the workspace).
+constexpr int kFieldsSmem = 48 * 1024;
 template <typename FT>
 __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_constant__ ShiftArgs args) {
+  extern __shared__ __align__(16) unsigned char fsmem[];
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int c = P.m > KF ? P.m - KF : 0;
@@ -566,8 +568,9 @@ __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_co
   const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
   FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
   const long long GC = 1ll << (2 * c);
-  FT* const bufA = wsf;                 // shifted-field area (3 * 4^c)
-  FT* const bufB = wsf + 6 * GC;        // scratch (3 * 4^(c-1))
+  const bool in_smem = (15ll * (GC / 16)) * (long long)sizeof(FT) <= kFieldsSmem;   // 3 (4^(c-1) + 4^(c-2))
+  FT* const bufA = in_smem ? reinterpret_cast<FT*>(fsmem) + 3 * (GC / 4) : wsf;        // level c-2, c-4, ...
+  FT* const bufB = in_smem ? reinterpret_cast<FT*>(fsmem) : wsf + 6 * GC;             // level c-1, c-3, ...
   FT* const fin = wsf + 3 * GC;         // unshifted level-c fields
   for (int l = 0; l < c; ++l) {
     const int gl = 1 << l, G2 = 2 * gl;
@@ -592,9 +595,15 @@ __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_co
         }
       FT Xl = FT(0), Yl = FT(0), Zl = FT(0);
       if (l > 0) {
-        Xl = __ldcg(cur + idx);
-        Yl = __ldcg(cur + gl * gl + idx);
-        Zl = __ldcg(cur + 2 * gl * gl + idx);
+        if (in_smem) {
+          Xl = cur[idx];
+          Yl = cur[gl * gl + idx];
+          Zl = cur[2 * gl * gl + idx];
+        } else {
+          Xl = __ldcg(cur + idx);
+          Yl = __ldcg(cur + gl * gl + idx);
+          Zl = __ldcg(cur + 2 * gl * gl + idx);
+        }
       }
       FT cx[2][2], cy[2][2], cz[2][2];
 #pragma unroll
@@ -651,12 +660,15 @@ __global__ void __launch_bounds__(kThreads) coarse_finish_kernel(const __grid_co
 
 template <typename FT>
 constexpr int max_tile_smem() {
-  int a = TSmem<FT, 3, 8>::BYTES, b = TSmem<FT, 3, 4>::BYTES;
-  return a > b ? a : b;
+  const int v[6] = {TSmem<FT, 3, 8>::BYTES, TSmem<FT, 3, 4>::BYTES, TSmem<FT, 3, 2>::BYTES,
+                    TSmem<FT, 3, 1>::BYTES, TSmem<FT, 2, 1>::BYTES, TSmem<FT, 1, 1>::BYTES};
+  int mx = 0;
+  for (int x : v) mx = x > mx ? x : mx;
+  return mx;
 }
 
 template <typename FT>
-__global__ void __launch_bounds__(kThreads, 2) shift2d_tile_kernel(const __grid_constant__ ShiftArgs args) {
+__global__ void __launch_bounds__(kThreads, sizeof(FT) == 4 ? 3 : 2) shift2d_tile_kernel(const __grid_constant__ ShiftArgs args) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int sR[2][2][HS_MAX_LOG2N + 1];
   __shared__ int sDoff[HS_MAX_LOG2N + 2];
@@ -725,13 +737,16 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
     HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_tile_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_tile_smem<FT>()),
                   "cudaFuncSetAttribute(shift2d_tile_kernel)");
+    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_fields_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFieldsSmem),
+                  "cudaFuncSetAttribute(coarse_fields_kernel)");
     HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_finish_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFinishSmem),
                   "cudaFuncSetAttribute(coarse_finish_kernel)");
     attr_done = true;
   }
   if (any_coarse) {
-    coarse_fields_kernel<FT><<<a.num_faces, kThreads, 0, st>>>(a);
+    coarse_fields_kernel<FT><<<a.num_faces, kThreads, kFieldsSmem, st>>>(a);
     HS_CHECK_LAUNCH("coarse_fields_kernel");
   }
   shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);
