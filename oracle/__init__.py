@@ -15,7 +15,12 @@ What it computes (DESIGN.md §2 lists every reading of the pap
   shift by box projection ("linear shift"), forward transform.
 * ``relight``: the double product R = T . L'  (PAPER.md eq:tripleSum P:265-266 with the Tripling
   Coefficient Theorem's scaling case P:287: C_{i j 0} = delta_ij) and the per-vertex
-  fused form r_v = <S_{s_v} L, T_v>.
+  fused form r_v = <S_{s_v} L, T_v>; the sparse gather and the triple
+  product as the pixel-domain triple integral (eq:tripleSum).
+* ``rotate``: rotation of lat-long maps by the spatial ground truth: inverse,
+  bilinear resampling at the rotated angles (eq:theta/eq:phi P:397-402), the azimuth shift,
+  forward; PSNR.  The GPU's chain-rule rotation approximates it (row f1): their agreement is a
+  PSNR, not a 1e-5 parity (R25).
 
 Everything is fp64 NumPy, written step by step with no blocking, fusion or reordering.
 Pins (tests/test_oracle_*.py, "-m 'not gpu'"): SPEC worked examples, dense
@@ -24,6 +29,6 @@ integrals <psi_i, T_s psi_j> for 1D N=8 and 2D 4x4, closed forms (identity at 0 
 composition, DC invariance, Parseval, linearity in the fractional part), SURVEY App. B examples.
 No function here is "parity unpinned".
 """
-from . import haar, shift, relight  # noqa: F401
+from . import haar, shift, relight, rotate  # noqa: F401
 
-__all__ = ["haar", "shift", "relight"]
+__all__ = ["haar", "shift", "relight", "rotate"]

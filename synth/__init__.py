@@ -31,7 +31,7 @@ __all__ = [
     "SEED_BASE", "STREAM_T", "shading_rows", "STREAM_BRDF", "STREAM_VIS", "splitmix64", "hash_u64", "hash_uniform", "level_of_index_2d",
     "level_of_index_1d", "transfer_rows", "light_pyramids", "random_signals", "CONFIGS",
     "Config", "config", "c1_shifts_1d", "c1_shifts_2d", "c3_shifts", "c4_vertex_shifts",
-    "c5_shifts",
+    "c5_shifts", "smooth_sphere_maps", "smooth_sphere_cell_means", "rotation_angles",
 ]
 
 SEED_BASE = 1705072720          # base seed 1705072720 + config index
@@ -213,6 +213,81 @@ def light_pyramids(seed: int, batch: int, faces: int, log2n: int, suns: int = 3)
                 c[base:4 * base] = (det * (2.0 ** -l)).reshape(-1)
             out[b, f] = c.astype(np.float32)
     return out
+
+
+def _interval_means(kind: str, p: int, lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
+    """Mean of cos(p x) (kind 'c') or sin(p x) (kind 's') over [lo, hi] in closed form."""
+    if p == 0:
+        return np.full(lo.shape, 1.0 if kind == "c" else 0.0)
+    if kind == "c":
+        return (np.sin(p * hi) - np.sin(p * lo)) / (p * (hi - lo))
+    return (np.cos(p * lo) - np.cos(p * hi)) / (p * (hi - lo))
+
+
+def _smooth_terms(seed: int, k: int, order: int):
+    rng = np.random.default_rng([seed, 0x5F, k])
+    terms = [("c", 0, "c", 0, 1.0)]
+    for p in range(order + 1):
+        for q in range(order + 1):
+            if p == 0 and q == 0:
+                continue
+            amp = 0.35 / (1.0 + p + q)
+            for kt in ("c", "s"):
+                for kp in ("c", "s"):
+                    if (p == 0 and kt == "s") or (q == 0 and kp == "s"):
+                        continue
+                    terms.append((kt, p, kp, q, float(rng.normal(0.0, amp))))
+    return terms
+
+
+def smooth_sphere_maps(seed: int, count: int, log2n: int, order: int = 3) -> np.ndarray:
+    """Smooth lat-long maps (rows theta in [0, pi] top first, columns phi in [0, 2 pi)) as HAAR1
+    pyramids, fp32 [count][N*N] -- BRDF-like inputs of the rotation row f1.
+
+    f(theta, phi) = 1 + sum_{p, q <= order} a_pq T_p(theta) S_q(phi), T/S in {cos, sin}, random
+    a_pq ~ N(0, (0.35 / (1 + p + q))^2).  Coefficients are exact cell integrals (closed-form means
+    of cos / sin over the dyadic intervals), combined per the Haar definition (detail = signed
+    quadrant-mean difference / 4, times 2**-l) -- no transform is run."""
+    n = log2n
+    N = 1 << n
+    out = np.empty((count, N * N), dtype=np.float32)
+    for kidx in range(count):
+        c = np.zeros(N * N, dtype=np.float64)
+        for kt, p, kp, q, a in _smooth_terms(seed, kidx, order):
+            def means(kind, freq, length, cells):
+                e = np.arange(cells + 1, dtype=np.float64) * (length / cells)
+                return _interval_means(kind, freq, e[:-1], e[1:])
+            c[0] += a * means(kt, p, math.pi, 1)[0] * means(kp, q, 2 * math.pi, 1)[0]
+            for l in range(n):
+                uc = means(kt, p, math.pi, 2 << l)
+                wc = means(kp, q, 2 * math.pi, 2 << l)
+                u0, u1, w0, w1 = uc[0::2], uc[1::2], wc[0::2], wc[1::2]
+                sc = a * 0.25 * 2.0 ** -l
+                base = 4 ** l
+                c[base:2 * base] += sc * np.outer(u0 + u1, w0 - w1).reshape(-1)
+                c[2 * base:3 * base] += sc * np.outer(u0 - u1, w0 + w1).reshape(-1)
+                c[3 * base:4 * base] += sc * np.outer(u0 - u1, w0 - w1).reshape(-1)
+        out[kidx] = c.astype(np.float32)
+    return out
+
+
+def smooth_sphere_cell_means(seed: int, count: int, log2n: int, order: int = 3) -> np.ndarray:
+    """The finest-level cell means of the same maps, fp64 [count][N][N] (test pin of the above)."""
+    N = 1 << log2n
+    out = np.zeros((count, N, N))
+    e_t = np.arange(N + 1, dtype=np.float64) * (math.pi / N)
+    e_p = np.arange(N + 1, dtype=np.float64) * (2 * math.pi / N)
+    for kidx in range(count):
+        for kt, p, kp, q, a in _smooth_terms(seed, kidx, order):
+            out[kidx] += a * np.outer(_interval_means(kt, p, e_t[:-1], e_t[1:]), _interval_means(kp, q, e_p[:-1], e_p[1:]))
+    return out
+
+
+def rotation_angles(seed: int, count: int) -> np.ndarray:
+    """Per-map rotations (alpha = elevation about X, beta = azimuth) in radians, fp64 [count][2]:
+    alpha ~ U[-pi/3, pi/3], beta ~ U[0, 2 pi) (row f1)."""
+    rng = np.random.default_rng([seed, 0xA7])
+    return np.stack([rng.uniform(-math.pi / 3, math.pi / 3, count), rng.uniform(0.0, 2 * math.pi, count)], axis=1)
 
 
 def random_signals(seed: int, count: int, size: int, kind: str = "normal") -> np.ndarray:

@@ -1,0 +1,83 @@
+"""Pins of the rotation oracle and of the smooth-map generator, -m "not gpu".
+
+* rotated angles: SPEC.md S:185 (alpha = 20 deg at (pi/2, 0) -> (pi/2 + 20 deg, 0)), identity,
+  the inverse rotation, orthogonality of R_x (great-circle distances preserved);
+* elevate_pixels: identity is an exact copy, constants stay constant, alpha = pi maps the map to
+  itself upside down with phi mirrored through pi (closed form);
+* rotate_coeffs: alpha = 0 with an integer azimuth shift is the exact circular column shift of the
+  pixel map, and alpha = 0, beta = 0 is the identity on coefficients;
+* synth.smooth_sphere_maps equals the forward transform of its closed-form cell means.
+"""
+import math
+
+import numpy as np
+
+import synth
+from oracle import haar, rotate
+
+
+def test_rotated_angles_examples():
+    a = math.radians(20.0)
+    Th, Ph = rotate.rotated_angles(math.pi / 2, 0.0, a)
+    assert abs(Th - (math.pi / 2 + a)) < 1e-12 and abs(Ph) < 1e-12
+    th = np.linspace(0.1, 3.0, 7)
+    ph = np.linspace(0.2, 6.0, 7)
+    T0, P0 = rotate.rotated_angles(th, ph, 0.0)
+    np.testing.assert_allclose(T0, th, atol=1e-12)
+    np.testing.assert_allclose(P0, ph, atol=1e-12)
+    T1, P1 = rotate.rotated_angles(th, ph, 0.7)
+    T2, P2 = rotate.rotated_angles(T1, P1, -0.7)
+    np.testing.assert_allclose(T2, th, atol=1e-10)
+    np.testing.assert_allclose(np.mod(P2 - ph + np.pi, 2 * np.pi) - np.pi, 0.0, atol=1e-10)
+
+
+def _dir(t, p):
+    return np.stack([np.sin(t) * np.sin(p), np.cos(t), np.sin(t) * np.cos(p)], axis=-1)
+
+
+def test_rotation_preserves_angles_between_points():
+    rng = np.random.default_rng(0)
+    t = rng.uniform(0.05, 3.0, (2, 50))
+    p = rng.uniform(0.0, 6.2, (2, 50))
+    T, P = rotate.rotated_angles(t, p, -1.1)
+    before = np.sum(_dir(t[0], p[0]) * _dir(t[1], p[1]), axis=-1)
+    after = np.sum(_dir(T[0], P[0]) * _dir(T[1], P[1]), axis=-1)
+    np.testing.assert_allclose(after, before, atol=1e-12)
+
+
+def test_elevate_identity_constant_and_half_turn():
+    rng = np.random.default_rng(1)
+    N = 16
+    f = rng.normal(size=(N, N))
+    np.testing.assert_allclose(rotate.elevate_pixels(f, 0.0), f, atol=1e-12)
+    np.testing.assert_allclose(rotate.elevate_pixels(np.full((N, N), 2.5), 0.9), 2.5, atol=1e-12)
+    # alpha = pi: (theta, phi) -> (pi - theta, pi - phi): row r -> N-1-r, column c -> N/2-1-c (mod N)
+    g = rotate.elevate_pixels(f, math.pi)
+    want = f[::-1][:, (N // 2 - 1 - np.arange(N)) % N]
+    np.testing.assert_allclose(g, want, atol=1e-9)
+
+
+def test_rotate_coeffs_identity_and_integer_azimuth():
+    c = synth.smooth_sphere_maps(7, 1, 4)[0].astype(np.float64)
+    np.testing.assert_allclose(rotate.rotate_coeffs(c, 0.0, 0.0), c, atol=1e-12)
+    N = 16
+    pix = haar.inverse2d(c)
+    got = haar.inverse2d(rotate.rotate_coeffs(c, 0.0, 3 * 2 * math.pi / N))
+    np.testing.assert_allclose(got, np.roll(pix, 3, axis=1), atol=1e-12)      # f'(x) = f(x - 3)
+
+
+def test_psnr_definition():
+    c = synth.smooth_sphere_maps(8, 1, 3)[0].astype(np.float64)
+    assert rotate.psnr(c, c) == float("inf")
+    d = c.copy()
+    d[0] += 0.01                                       # every pixel moves by 0.01
+    peak = np.abs(haar.inverse2d(c)).max()
+    assert abs(rotate.psnr(d, c) - 10 * np.log10(peak ** 2 / 1e-4)) < 1e-9
+
+
+def test_smooth_maps_are_cell_integrals():
+    for n in (3, 5):
+        c = synth.smooth_sphere_maps(3, 2, n)
+        m = synth.smooth_sphere_cell_means(3, 2, n)
+        for k in range(2):
+            np.testing.assert_allclose(haar.forward2d(m[k]), c[k], atol=3e-7)
