@@ -234,6 +234,32 @@ HS_API hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64
                                  float* out, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * haar_rotate_coeffs -- rotation of lat-long maps directly on their Haar coefficients (SURVEY.md
+ * §8(f) f1; the paper's "non-linear phase shift").
+ *
+ * Defines:  P:350-459 (eq:theta/eq:phi P:397-402: g(theta, phi) = f(Theta, Phi); chain rule
+ *           eq:pde1-2 P:416-425 on the coefficients' difference fields), recursion to coarser
+ *           levels P:466-497/"rotation around the x-axis followed by a simple shifting along
+ *           the phi-axis" P:459/P:508.
+ *
+ *   in, out       DEVICE [batch][N*N] fp32 HAAR1 pyramids of N x N lat-long maps (rows theta in
+ *                 [0, pi] top first, columns phi in [0, 2 pi)); in and out must not overlap.
+ *   angles_host   HOST [batch][2] fp64: (alpha, beta) radians -- elevation about X with the active
+ *                 matrix R_x(alpha) = [[1,0,0],[0,cos,-sin],[0,sin,cos]] applied as
+ *                 g(theta, phi) = f(angles of R_x p), then the shift along phi by beta N / (2 pi)
+ *                 columns (f'(x) = f(x - s), exact, as haar_shift_coeffs).
+ *   log2n         1 .. 11.   workspace >= haar_rotate_workspace_bytes(log2n, batch), 16-byte aligned.
+ *   Accuracy: the elevation is the paper's first-order chain rule on the finest-level difference
+ *   fields with bilinear resampling (approximate by construction: compared with the spatial
+ *   ground truth as PSNR, R25-R27); alpha = 0 reproduces the input to fp32 rounding
+ *   and the azimuth part is exact.
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status haar_rotate_coeffs(const float* in, float* out, int log2n, int batch, const double* angles_host,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+HS_API size_t haar_rotate_workspace_bytes(int log2n, int batch);
+
+/* ---------------------------------------------------------------------------------------------
  * hs_fill_transfer -- seeded synthetic transfer rows, generated in place (input generator, not
  * part of the method; bit-identical to synth.transfer_rows):
  *   T[v][f*k_face + k] = u * 2^-level(k), u = ((h >> 40) - 2^23) / 2^23,

@@ -11,6 +11,7 @@ device memory and streams.  Function names follow the C ABI:
 * ``relight_vertices_triple``  triple product, BRDF and visibility separate (f3);
   ``haar_pack_qtree`` converts HAAR1 pyramids to its qtree storage layout
 * ``haar_shift_coeffs_coarse`` coarse-start shift (f4)
+* ``haar_rotate_coeffs``       rotation of lat-long maps in the Haar domain (f1)
 * ``hs_fill_transfer``         seeded synthetic transfer rows generated in place (input generator)
 
 See DESIGN.md for the method, its readings of the paper, layouts and kernels.
@@ -20,6 +21,8 @@ from __future__ import annotations
 from ._lib import HaarShiftError, load  # noqa: F401
 from .api import (  # noqa: F401
     haar_pack_qtree,
+    haar_rotate_coeffs,
+    haar_rotate_workspace_bytes,
     haar_shift_coarse_workspace_bytes,
     haar_shift_coeffs,
     haar_shift_coeffs_coarse,
@@ -43,4 +46,5 @@ __all__ = [
     "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
     "shift_and_relight", "hs_fill_sparse_transfer", "relight_vertices_sparse",
     "relight_sparse_workspace_bytes", "haar_pack_qtree", "relight_triple_workspace_bytes", "relight_vertices_triple",
+    "haar_rotate_coeffs", "haar_rotate_workspace_bytes",
 ]

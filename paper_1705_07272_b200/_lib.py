@@ -37,6 +37,9 @@ SIGNATURES = {
     "relight_triple_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int, _c.c_int, _c.c_int]),
     "haar_pack_qtree": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int, _c.c_int64, _c.c_int, _c.c_void_p,
                                    _c.c_void_p]),
+    "haar_rotate_coeffs": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p,
+                                      _c.c_size_t, _c.c_void_p]),
+    "haar_rotate_workspace_bytes": (_c.c_size_t, [_c.c_int, _c.c_int]),
     "hs_last_launch_count": (_c.c_int, []),
     "hs_status_string": (_c.c_char_p, [_c.c_int]),
     "hs_last_cuda_error": (_c.c_char_p, []),

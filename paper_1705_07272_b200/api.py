@@ -105,6 +105,35 @@ def haar_shift_coeffs_coarse(coeffs: torch.Tensor, shifts, start_level: int, ban
     return out
 
 
+def haar_rotate_workspace_bytes(log2n: int, batch: int) -> int:
+    return int(load().haar_rotate_workspace_bytes(log2n, batch))
+
+
+def haar_rotate_coeffs(coeffs: torch.Tensor, angles, out: Optional[torch.Tensor] = None,
+                       workspace: Optional[torch.Tensor] = None,
+                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """coeffs [batch][N*N] (HAAR1 lat-long maps) -> rotated pyramids [batch][N*N]; angles host
+    [batch][2] (alpha elevation about X, beta azimuth) in radians (include/haarshift.h)."""
+    lib = load()
+    _dev_f32(coeffs, "coeffs")
+    B = coeffs.shape[0]
+    K = coeffs.numel() // B
+    n = (int(K).bit_length() - 1) // 2
+    if 4 ** n != K:
+        raise ValueError("maps must hold 4**log2n coefficients")
+    ang = np.ascontiguousarray(np.asarray(angles, dtype=np.float64).reshape(B, 2))
+    if out is None:
+        out = torch.empty_like(coeffs)
+    _dev_f32(out, "out")
+    need = haar_rotate_workspace_bytes(n, B)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
+    st = lib.haar_rotate_coeffs(coeffs.data_ptr(), out.data_ptr(), n, B, ang.ctypes.data_as(ctypes.c_void_p),
+                                workspace.data_ptr(), need, _stream_ptr(stream))
+    check("haar_rotate_coeffs", st)
+    return out
+
+
 def relight_workspace_bytes(faces: int, k_face: int, batch: int) -> int:
     return int(load().relight_workspace_bytes(faces, k_face, batch))
 

@@ -254,6 +254,30 @@ hs_status relight_vertices_sparse(const int32_t* indices, const float* values, i
   return s;
 }
 
+size_t haar_rotate_workspace_bytes(int log2n, int batch) {
+  if (log2n < 1 || log2n > 11 || batch < 1) return 0;
+  return rotate_workspace_bytes_impl(log2n, batch);
+}
+
+hs_status haar_rotate_coeffs(const float* in, float* out, int log2n, int batch, const double* angles_host,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!in || !out || !angles_host || !workspace) return HS_ERR_INVALID_ARG;
+  if (log2n < 1 || log2n > 11 || batch < 1) return HS_ERR_INVALID_ARG;
+  for (long long i = 0; i < 2ll * batch; ++i)
+    if (!std::isfinite(angles_host[i])) return HS_ERR_INVALID_ARG;
+  const size_t K = (size_t)1 << (2 * log2n);
+  if (overlap(in, (size_t)batch * K * 4, out, (size_t)batch * K * 4)) return HS_ERR_INVALID_ARG;
+  if (workspace_bytes < rotate_workspace_bytes_impl(log2n, batch)) return HS_ERR_INVALID_ARG;
+  if (!aligned16(in) || !aligned16(out) || !aligned16(workspace)) return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_rotate(in, out, log2n, batch, angles_host, workspace, workspace_bytes, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
 hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64_t in_face_stride, int log2k, float* out,
                           void* stream) {
   g_last_launches = 0;

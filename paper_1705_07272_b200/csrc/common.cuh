@@ -167,6 +167,9 @@ size_t relight_triple_workspace_bytes_impl(long long V, int faces, int kface, in
 hs_status launch_relight_triple(const float* brdf_q, const float* vis_q, long long V, int faces, int kface,
                                 const float* light, long long lstride, int batch, float* R, void* ws, size_t ws_bytes,
                                 cudaStream_t st);
+size_t rotate_workspace_bytes_impl(int log2n, long long maps);
+hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
+                        size_t ws_bytes, cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
                                int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
 

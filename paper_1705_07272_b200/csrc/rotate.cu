@@ -1,0 +1,401 @@
+// Rotation of lat-long maps in the Haar domain: the paper's non-linear
+// phase shift (algorithm).  A rotation is an elevation about X
+// followed by a shift along phi; the elevation is done by the chain rule on the
+// coefficients' difference fields, the shift by the exact Haar-domain shift
+// (shift2d.cu).  DESIGN.md §5.9 and readings R25-R27.
+//
+// Map: N x N, row r at theta_r = (r + 1/2) pi / N (top first), column c at phi_c = (c + 1/2) 2 pi / N,
+// p = (sin t sin f, cos t, sin t cos f); the elevation maps g(theta, phi) = f(Theta, Phi) with
+// Theta = acos(R_2 p), Phi = atan2(R_1 p, R_3 p) for p' = R_x(alpha) p (eq:theta/eq:phi P:397-402).
+//
+//   rot_topdown_kernel   (1) the fields of f at the finest level from the detail coefficients
+//                        only, level by level (X = A[i][j] - A[i][j+1], Y = A[i][j] - A[i+1][j]);
+//   rot_pole_kernel      the rows of the fields across the poles (reflection: the row beyond a pole
+//                        is the pole row seen from phi + pi), from the pole rows of X_f;
+//   rot_chainrule_kernel (2) per output difference: X_g[i][j] = g(theta_i, phi_j) - g(theta_i, phi_j+1)
+//                        and Y_g[i][j] = g(theta_i, phi_j) - g(theta_i+1, phi_j) by the chain rule
+//                        (eq:pde1-2 P:416-425) with the angle increments of the two rotated
+//                        samples:  dg = f_Theta dTheta + f_Phi dPhi, f_Theta = -Y_f / dtheta and
+//                        f_Phi = -X_f / dphi interpolated bilinearly at the rotated midpoint
+//                        (Fig. 4; R26 -- increments instead of derivatives
+//                        keep the poles of the source finite);
+//   rot_closure_kernel   the periodic closure the Haar fields satisfy (rows of X and columns of Y
+//                        sum to zero; the Y row across the pole wrap is the negative column sum);
+//   rot_bottomup_kernel  (3) the paper's recursion h_s = [1,1], h_t = [1,2,1], decimated by 2
+//                        (eq:conv-sker P:466-478) from (X_g, Y_g, Z_g = X_g[i] - X_g[i+1])
+//                        at the finest level down to level 0: every detail coefficient of g;
+//   rot_dc_kernel        the scaling coefficient: mean of the level-L approximation of f
+//                        (L = min(n, 6), partial top-down in shared memory) resampled at the rotated
+//                        positions of the N x N grid (the paper is silent);
+// then haar_shift's kernels move the result by beta N / (2 pi) columns.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hs {
+namespace {
+
+constexpr int kRotChunk = 1024;   // maps per launch sequence (angles travel as kernel parameters)
+constexpr int kDcLevel = 6;
+
+struct RotParams {
+  float ca[kRotChunk];
+  float sa[kRotChunk];
+};
+
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// ------------------------------------------------------------------------------- (1) top-down
+// level l -> l+1 for all maps: fields [map][2][4^l] (X, Y) in cur, [map][2][4^(l+1)] in nxt.
+__global__ void rot_topdown_kernel(const float* __restrict__ in, long long maps, int n, int l,
+                                   const float* __restrict__ cur, float* __restrict__ nxt) {
+  const int g = 1 << l, G2 = 2 * g;
+  const long long per = 1ll << (2 * l);
+  const long long total = maps * per;
+  const long long NN = 1ll << (2 * n);
+  const float asc = pow2f(l);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e >> (2 * l);
+    const int cell = (int)(e & (per - 1));
+    const int i = cell >> l, j = cell & (g - 1);
+    const float* src = in + b * NN;
+    float d[3][4];  // cells (i,j), (i,j+1), (i+1,j): delta_00, delta_01, delta_10, delta_11
+    const int cells[3] = {cell, i * g + ((j + 1) & (g - 1)), ((i + 1) & (g - 1)) * g + j};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float H = __ldg(src + per + cells[k]) * asc;
+      const float V = __ldg(src + 2 * per + cells[k]) * asc;
+      const float D = __ldg(src + 3 * per + cells[k]) * asc;
+      d[k][0] = H + V + D;
+      d[k][1] = -H + V - D;
+      d[k][2] = H - V - D;
+      d[k][3] = -H - V + D;
+    }
+    float Xl = 0.f, Yl = 0.f;
+    if (l > 0) {
+      Xl = cur[b * 2 * per + cell];
+      Yl = cur[b * 2 * per + per + cell];
+    }
+    float* X = nxt + b * 8 * per;          // [2][4 per]
+    float* Y = X + 4 * per;
+    const int r0 = 2 * i, c0 = 2 * j;
+    // X[2i+a][2j] = d_a0 - d_a1 ;  X[2i+a][2j+1] = X_l + d_a1 - d_a0(i, j+1)
+    X[r0 * G2 + c0] = d[0][0] - d[0][1];
+    X[(r0 + 1) * G2 + c0] = d[0][2] - d[0][3];
+    X[r0 * G2 + c0 + 1] = Xl + d[0][1] - d[1][0];
+    X[(r0 + 1) * G2 + c0 + 1] = Xl + d[0][3] - d[1][2];
+    // Y[2i][2j+b] = d_0b - d_1b ;  Y[2i+1][2j+b] = Y_l + d_1b - d_0b(i+1, j)
+    Y[r0 * G2 + c0] = d[0][0] - d[0][2];
+    Y[r0 * G2 + c0 + 1] = d[0][1] - d[0][3];
+    Y[(r0 + 1) * G2 + c0] = Yl + d[0][2] - d[2][0];
+    Y[(r0 + 1) * G2 + c0 + 1] = Yl + d[0][3] - d[2][1];
+  }
+}
+
+// ------------------------------------------------------------------------------- (2) chain rule
+struct Jac {
+  float Th, Ph;          // rotated angles
+  float Tt, Tp, Pt, Pp;  // dTheta/dtheta, dTheta/dphi, dPhi/dtheta, dPhi/dphi
+};
+
+__device__ __forceinline__ Jac rotated(float th, float ph, float ca, float sa) {
+  float st, ct, sp, cp;
+  sincosf(th, &st, &ct);
+  sincosf(ph, &sp, &cp);
+  const float a = st * sp;                   // x' = x
+  const float u = ca * ct - sa * st * cp;    // y' = cos Theta
+  const float b = sa * ct + ca * st * cp;    // z'
+  Jac J;
+  J.Th = acosf(fminf(1.f, fmaxf(-1.f, u)));
+  float P = atan2f(a, b);
+  if (P < 0.f) P += 6.283185307179586f;
+  J.Ph = P;
+  const float s2 = fmaxf(a * a + b * b, 1e-12f);   // sin^2 Theta
+  const float is = rsqrtf(s2);
+  const float u_t = -ca * st - sa * ct * cp, u_p = sa * st * sp;
+  J.Tt = -u_t * is;
+  J.Tp = -u_p * is;
+  const float a_t = ct * sp, a_p = st * cp;
+  const float b_t = -sa * st + ca * ct * cp, b_p = -ca * st * sp;
+  J.Pt = (b * a_t - a * b_t) / s2;
+  J.Pp = (b * a_p - a * b_p) / s2;
+  return J;
+}
+
+// bilinear sample of a field plane (rows 0..R-1) extended by the reflected rows lo (row -1) and
+// hi (row R) at index coordinates (y, x), periodic in x
+__device__ __forceinline__ float sample_ext(const float* __restrict__ P, const float* __restrict__ lo,
+                                           const float* __restrict__ hi, int N, int R, float y, float x) {
+  y = fminf(fmaxf(y, -1.f), (float)R);
+  const float fy = floorf(y), fx = floorf(x);
+  const float wy = y - fy, wx = x - fx;
+  const int y0 = (int)fy, y1 = min(y0 + 1, R);
+  const int x0 = ((int)fx) & (N - 1), x1 = (x0 + 1) & (N - 1);
+  const float* r0 = y0 < 0 ? lo : (y0 >= R ? hi : P + y0 * N);
+  const float* r1 = y1 < 0 ? lo : (y1 >= R ? hi : P + y1 * N);
+  return (1.f - wy) * ((1.f - wx) * __ldg(r0 + x0) + wx * __ldg(r0 + x1)) +
+         wy * ((1.f - wx) * __ldg(r1 + x0) + wx * __ldg(r1 + x1));
+}
+
+// pole rows per map: E [map][4][N] = X row -1, X row N, Y row -1, Y row N-1 (reflected)
+__global__ void rot_pole_kernel(const float* __restrict__ F, int n, float* __restrict__ E) {
+  const int N = 1 << n, h = N / 2;
+  const long long NN = 1ll << (2 * n);
+  const float* X = F + (long long)blockIdx.x * 2 * NN;
+  float* e = E + (long long)blockIdx.x * 4 * N;
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    e[c] = X[(c + h) & (N - 1)];                              // X(theta_-1, phi) = X(theta_0, phi + pi)
+    e[N + c] = X[(N - 1) * N + ((c + h) & (N - 1))];
+    float s0 = 0.f, s1 = 0.f;                                  // A[r][c] - A[r][c + N/2] by telescoping X
+    for (int k = 0; k < h; ++k) {
+      s0 += X[(c + k) & (N - 1)];
+      s1 += X[(N - 1) * N + ((c + k) & (N - 1))];
+    }
+    e[2 * N + c] = -s0;                                        // A[-1][c] - A[0][c] = A[0][c+N/2] - A[0][c]
+    e[3 * N + c] = s1;                                         // A[N-1][c] - A[N][c]
+  }
+}
+
+// f's fields F [map][2][N][N] (X_f, Y_f) + pole rows E; g's fields out: G [map][2][N][N]
+__global__ void rot_chainrule_kernel(const float* __restrict__ F, const float* __restrict__ E, long long maps, int n,
+                                     const __grid_constant__ RotParams prm, float* __restrict__ Gf) {
+  const int N = 1 << n;
+  const long long NN = 1ll << (2 * n);
+  const long long total = maps * NN;
+  const float kT = 3.14159265358979f / (float)N, kP = 6.283185307179586f / (float)N;
+  const float iT = (float)N / 3.14159265358979f, iP = (float)N / 6.283185307179586f;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e >> (2 * n);
+    const int pix = (int)(e & (NN - 1));
+    const int i = pix >> n, j = pix & (N - 1);
+    const float ca = prm.ca[b], sa = prm.sa[b];
+    const float* Xf = F + b * 2 * NN;
+    const float* Yf = Xf + NN;
+    const float* Eb = E + b * 4 * N;
+    const Jac A0 = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
+      const float di = t ? 1.f : 0.f, dj = t ? 0.f : 1.f;
+      const Jac A1 = rotated(((float)i + 0.5f + di) * kT, ((float)j + 0.5f + dj) * kP, ca, sa);
+      const Jac M = rotated(((float)i + 0.5f + 0.5f * di) * kT, ((float)j + 0.5f + 0.5f * dj) * kP, ca, sa);
+      const float y = M.Th * iT - 0.5f, x = M.Ph * iP - 0.5f;
+      const float xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5f);           // X_f lives at (i, j + 1/2)
+      const float yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5f, x);  // Y_f at (i + 1/2, j)
+      const float dT = A0.Th - A1.Th;
+      float dP = A0.Ph - A1.Ph;
+      if (dP > 3.14159265358979f) dP -= 6.283185307179586f;
+      if (dP < -3.14159265358979f) dP += 6.283185307179586f;
+      Gf[b * 2 * NN + t * NN + pix] = -yf * dT * iT - xf * dP * iP;
+    }
+  }
+}
+
+// closure: rows of X_g sum to 0 (subtract the row mean); column j of Y_g: last row = -sum of the
+// others.  One CTA per map; a warp per row (coalesced), a thread per column (coalesced).
+__global__ void rot_closure_kernel(float* __restrict__ Gf, int n) {
+  const int N = 1 << n;
+  const long long NN = 1ll << (2 * n);
+  float* X = Gf + (long long)blockIdx.x * 2 * NN;
+  float* Y = X + NN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < N; r += nw) {
+    float sx = 0.f;
+    for (int t = lane; t < N; t += 32) sx += X[r * N + t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    const float mx = sx / (float)N;
+    for (int t = lane; t < N; t += 32) X[r * N + t] -= mx;
+  }
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    float sy = 0.f;
+    for (int t = 0; t < N - 1; ++t) sy += Y[t * N + k];
+    Y[(N - 1) * N + k] = -sy;
+  }
+}
+
+// ------------------------------------------------------------------------------- (3) bottom-up
+// from fields at level l+1 (src: [map][planes][4^(l+1)]; at the finest level planes = 2 and
+// Z = X[i] - X[i+1]) to level l (dst [map][3][4^l]) and the level-l details of the output pyramid.
+__global__ void rot_bottomup_kernel(const float* __restrict__ src, int src_planes, long long maps, int l,
+                                    float* __restrict__ dst, float* __restrict__ out, int n) {
+  const int g = 1 << l, G2 = 2 * g;
+  const long long per = 1ll << (2 * l), sper = 4 * per;
+  const long long total = maps * per;
+  const long long NN = 1ll << (2 * n);
+  const float q = 0.25f, osc = pow2f(-l);
+  const bool zfromx = (src_planes == 2);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e >> (2 * l);
+    const int cell = (int)(e & (per - 1));
+    const int i = cell >> l, j = cell & (g - 1);
+    const float* X = src + b * src_planes * sper;
+    const float* Y = X + sper;
+    const int rr[4] = {2 * i, 2 * i + 1, (2 * i + 2) & (G2 - 1), (2 * i + 3) & (G2 - 1)};
+    const int cc[3] = {2 * j, 2 * j + 1, (2 * j + 2) & (G2 - 1)};
+    auto x = [&](int u, int w) { return X[rr[u] * G2 + cc[w]]; };
+    auto y = [&](int u, int w) { return Y[rr[u] * G2 + cc[w]]; };
+    auto z = [&](int u, int w) {
+      return zfromx ? X[rr[u] * G2 + cc[w]] - X[rr[u + 1] * G2 + cc[w]] : X[2 * sper + rr[u] * G2 + cc[w]];
+    };
+    const float Xn = q * (x(0, 0) + 2.f * x(0, 1) + x(0, 2) + x(1, 0) + 2.f * x(1, 1) + x(1, 2));
+    const float Yn = q * (y(0, 0) + 2.f * y(1, 0) + y(2, 0) + y(0, 1) + 2.f * y(1, 1) + y(2, 1));
+    const float Zn = q * ((z(0, 0) + 2.f * z(0, 1) + z(0, 2)) + 2.f * (z(1, 0) + 2.f * z(1, 1) + z(1, 2)) +
+                          (z(2, 0) + 2.f * z(2, 1) + z(2, 2)));
+    float* D = dst + b * 3 * per;
+    D[cell] = Xn;
+    D[per + cell] = Yn;
+    D[2 * per + cell] = Zn;
+    float* o = out + b * NN;
+    o[per + cell] = q * (x(0, 0) + x(1, 0)) * osc;
+    o[2 * per + cell] = q * (y(0, 0) + y(0, 1)) * osc;
+    o[3 * per + cell] = q * z(0, 0) * osc;
+  }
+}
+
+// ------------------------------------------------------------------------------- scaling
+__global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ in, int n, long long map0,
+                                                     const __grid_constant__ RotParams prm, float* __restrict__ out) {
+  __shared__ float A[2][1 << (2 * kDcLevel)];
+  __shared__ float red[8];
+  const long long b = blockIdx.x;
+  const long long NN = 1ll << (2 * n);
+  const float* src = in + b * NN;
+  const int L = n < kDcLevel ? n : kDcLevel;
+  if (threadIdx.x == 0) A[0][0] = __ldg(src);
+  __syncthreads();
+  int cb = 0;
+  for (int l = 0; l < L; ++l) {  // A_{l+1}[2i+a][2j+b] = A_l + delta_ab (averaging details = 2^l x unit)
+    const int g = 1 << l, per = g * g;
+    const float asc = pow2f(l);
+    for (int cell = threadIdx.x; cell < per; cell += blockDim.x) {
+      const int i = cell >> l, j = cell & (g - 1);
+      const float H = __ldg(src + per + cell) * asc, V = __ldg(src + 2 * per + cell) * asc,
+                  D = __ldg(src + 3 * per + cell) * asc;
+      const float a = A[cb][cell];
+      float* nx = A[cb ^ 1];
+      nx[(2 * i) * 2 * g + 2 * j] = a + H + V + D;
+      nx[(2 * i) * 2 * g + 2 * j + 1] = a - H + V - D;
+      nx[(2 * i + 1) * 2 * g + 2 * j] = a + H - V - D;
+      nx[(2 * i + 1) * 2 * g + 2 * j + 1] = a - H - V + D;
+    }
+    __syncthreads();
+    cb ^= 1;
+  }
+  const int M = 1 << L;
+  const int N = 1 << n;
+  const float ca = prm.ca[map0 + b], sa = prm.sa[map0 + b];
+  const float kT = 3.14159265358979f / (float)N, kP = 6.283185307179586f / (float)N;
+  float acc = 0.f;
+  for (long long p = threadIdx.x; p < NN; p += blockDim.x) {
+    const int i = (int)(p >> n), j = (int)(p & (N - 1));
+    const Jac J = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
+    const float y = J.Th * (float)M / 3.14159265358979f - 0.5f;   // in [-1/2, M - 1/2]
+    const float x = J.Ph * (float)M / 6.283185307179586f - 0.5f;
+    const float fy = floorf(y), fx = floorf(x);
+    const float wy = y - fy, wx = x - fx;
+    const float* P = A[cb];
+    auto at = [&](int r, int c) {  // rows beyond a pole: the pole row seen from phi + pi
+      if (r < 0) { r = -1 - r; c += M / 2; }
+      if (r >= M) { r = 2 * M - 1 - r; c += M / 2; }
+      return P[r * M + (c & (M - 1))];
+    };
+    const int y0 = (int)fy, x0 = (int)fx;
+    acc += (1.f - wy) * ((1.f - wx) * at(y0, x0) + wx * at(y0, x0 + 1)) +
+           wy * ((1.f - wx) * at(y0 + 1, x0) + wx * at(y0 + 1, x0 + 1));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    out[b * NN] = s / (float)NN;
+  }
+}
+
+unsigned grid_for(long long total) {
+  long long b = (total + 255) / 256;
+  if (b > 148ll * 32) b = 148ll * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+// Workspace: F ping-pong 2 x [maps][2][N^2], G [maps][2][N^2], tmp pyramid [maps][N^2], pole rows
+// [maps][4][N], then the shift's workspace.
+size_t rotate_workspace_bytes_impl(int log2n, long long maps) {
+  const size_t NN = (size_t)1 << (2 * log2n);
+  const size_t f = (size_t)maps * NN * sizeof(float);
+  const size_t pb = ((size_t)maps * 4 * ((size_t)1 << log2n) * sizeof(float) + 255) & ~size_t(255);
+  return 2 * 2 * f + 2 * f + f + pb + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
+}
+
+hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+  const long long NN = 1ll << (2 * n);
+  const size_t f = (size_t)maps * NN * sizeof(float);
+  char* base = reinterpret_cast<char*>(ws);
+  float* bufA = reinterpret_cast<float*>(base);
+  float* bufB = reinterpret_cast<float*>(base + 2 * f);
+  float* Gf = reinterpret_cast<float*>(base + 4 * f);
+  float* tmp = reinterpret_cast<float*>(base + 6 * f);
+  const size_t pb = ((size_t)maps * 4 * ((size_t)1 << n) * sizeof(float) + 255) & ~size_t(255);
+  float* poles = reinterpret_cast<float*>(base + 7 * f);
+  void* sws = base + 7 * f + pb;
+  const size_t sws_bytes = ws_bytes - 7 * f - pb;
+
+  for (long long m0 = 0; m0 < maps; m0 += kRotChunk) {
+    const long long mc = (maps - m0) < kRotChunk ? (maps - m0) : kRotChunk;
+    RotParams prm;
+    for (long long k = 0; k < mc; ++k) {
+      prm.ca[k] = (float)std::cos(angles[2 * (m0 + k)]);
+      prm.sa[k] = (float)std::sin(angles[2 * (m0 + k)]);
+    }
+    const float* src = in + m0 * NN;
+    float* dtmp = tmp + m0 * NN;
+    // (1) top-down to the finest fields (ping-pong between bufA and bufB)
+    float* cur = bufB;
+    for (int l = 0; l < n; ++l) {
+      float* nxt = (cur == bufA) ? bufB : bufA;
+      rot_topdown_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(src, mc, n, l, cur, nxt);
+      HS_CHECK_LAUNCH("rot_topdown_kernel");
+      cur = nxt;
+    }
+    // (2) pole rows, chain rule, closure
+    rot_pole_kernel<<<(unsigned)mc, 256, 0, st>>>(cur, n, poles);
+    HS_CHECK_LAUNCH("rot_pole_kernel");
+    rot_chainrule_kernel<<<grid_for(mc * NN), 256, 0, st>>>(cur, poles, mc, n, prm, Gf);
+    HS_CHECK_LAUNCH("rot_chainrule_kernel");
+    rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
+    HS_CHECK_LAUNCH("rot_closure_kernel");
+    // (3) bottom-up, every detail level of the rotated pyramid
+    const float* s = Gf;
+    int planes = 2;
+    float* d = bufA;
+    for (int l = n - 1; l >= 0; --l) {
+      rot_bottomup_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(s, planes, mc, l, d, dtmp, n);
+      HS_CHECK_LAUNCH("rot_bottomup_kernel");
+      s = d;
+      planes = 3;
+      d = (d == bufA) ? bufB : bufA;
+    }
+    rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, n, 0, prm, dtmp);
+    HS_CHECK_LAUNCH("rot_dc_kernel");
+  }
+  // azimuth: the exact shift by beta N / (2 pi) columns
+  std::vector<double> sh((size_t)maps * 2);
+  for (long long k = 0; k < maps; ++k) {
+    sh[2 * k] = 0.0;
+    sh[2 * k + 1] = angles[2 * k + 1] * (double)(1 << n) / 6.283185307179586;
+  }
+  return launch_shift(tmp, out, 2, n, 1, maps, NN, NN, sh.data(), nullptr, nullptr, n, sws, sws_bytes, st);
+}
+
+}  // namespace hs

@@ -31,7 +31,7 @@ __all__ = [
     "SEED_BASE", "STREAM_T", "shading_rows", "STREAM_BRDF", "STREAM_VIS", "splitmix64", "hash_u64", "hash_uniform", "level_of_index_2d",
     "level_of_index_1d", "transfer_rows", "light_pyramids", "random_signals", "CONFIGS",
     "Config", "config", "c1_shifts_1d", "c1_shifts_2d", "c3_shifts", "c4_vertex_shifts",
-    "c5_shifts", "smooth_sphere_maps", "smooth_sphere_cell_means", "rotation_angles",
+    "c5_shifts", "smooth_sphere_maps", "smooth_sphere_cell_means", "smooth_sphere_eval", "rotation_angles",
 ]
 
 SEED_BASE = 1705072720          # base seed 1705072720 + config index
@@ -283,6 +283,19 @@ def smooth_sphere_cell_means(seed: int, count: int, log2n: int, order: int = 3) 
     return out
 
 
+def smooth_sphere_eval(seed: int, k: int, theta, phi, order: int = 3) -> np.ndarray:
+    """Point values of map k of smooth_sphere_maps at (theta, phi) (fp64; the analytic ground truth
+    of the rotation tests)."""
+    theta = np.asarray(theta, dtype=np.float64)
+    phi = np.asarray(phi, dtype=np.float64)
+    out = np.zeros(np.broadcast(theta, phi).shape)
+    for kt, p, kp, q, a in _smooth_terms(seed, k, order):
+        u = np.cos(p * theta) if kt == "c" else np.sin(p * theta)
+        w = np.cos(q * phi) if kp == "c" else np.sin(q * phi)
+        out += a * u * w
+    return out
+
+
 def rotation_angles(seed: int, count: int) -> np.ndarray:
     """Per-map rotations (alpha = elevation about X, beta = azimuth) in radians, fp64 [count][2]:
     alpha ~ U[-pi/3, pi/3], beta ~ U[0, 2 pi) (row f1)."""
@@ -372,6 +385,8 @@ CONFIGS = {
     "c5s": Config("c5s", 8, 6, 1000000, 8, 64, SEED_BASE + 5,
                   "c5 with sparse top-K transfer (K_s = 256 full-resolution coefficients per vertex, row f2)",
                   {"k_sparse": 256, "dense_levels": 2}),
+    "c6r": Config("c6r", 6, 1, 0, 6, 4096, SEED_BASE + 6,
+                  "row f1: 4096 lat-long maps of 64 x 64 (BRDF-like, smooth), each rotated by its own (alpha, beta)"),
     "c5t": Config("c5t", 8, 6, 1000000, 5, 64, SEED_BASE + 5,
                   "c5 with the triple product (row f3): per-vertex BRDF and visibility, each 6 x 1024 coefficients"),
 }

@@ -81,3 +81,14 @@ def test_smooth_maps_are_cell_integrals():
         m = synth.smooth_sphere_cell_means(3, 2, n)
         for k in range(2):
             np.testing.assert_allclose(haar.forward2d(m[k]), c[k], atol=3e-7)
+
+
+def test_smooth_eval_matches_cell_means():
+    """the point evaluator integrates (Gauss-Legendre, 4 x 4 per cell) to the closed-form cell means"""
+    n, N = 4, 16
+    g, w = np.polynomial.legendre.leggauss(4)
+    th = (np.arange(N)[:, None] + 0.5 + 0.5 * g[None, :]) * np.pi / N        # [N][4]
+    ph = (np.arange(N)[:, None] + 0.5 + 0.5 * g[None, :]) * 2 * np.pi / N
+    vals = synth.smooth_sphere_eval(5, 1, th[:, None, :, None], ph[None, :, None, :])
+    means = np.einsum("rcab,a,b->rc", vals, w, w) / 4.0
+    np.testing.assert_allclose(means, synth.smooth_sphere_cell_means(5, 2, n)[1], atol=1e-9)
