@@ -54,6 +54,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunks", type=int, default=4)
     p.add_argument("--e2e-chunks", type=int, default=4)
+    p.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                   help="N>1: fused relight + gather into rank 0's buffer over NVLink (p2p) or NCCL gather")
     p.add_argument("--start-level", type=int, default=None,
                    help="coarse-start shift (row f4, approximate): shift the level-L approximation only")
     return p.parse_args()
@@ -238,6 +240,20 @@ def run_ours(args, cfg):
         raise SystemExit("--start-level is a single-GPU option")
     R = torch.empty((rows, B), dtype=torch.float32, device=dev)
     R_full = torch.empty((V, B), dtype=torch.float32, device=dev) if (rank == 0 and world > 1) else None
+    gather_mode = args.gather if world > 1 else "none"
+    R_view = None
+    if gather_mode == "p2p":
+        # fused relight + gather: every rank's relight epilogue stores straight into rank 0's buffer
+        try:
+            R_view = hsdist.open_peer_view(R_full, (V, B), dev)
+        except Exception as e:  # devices cannot reach each other: NCCL gather instead
+            if rank == 0:
+                print(f"[bench] p2p gather unavailable ({e!r}); using the NCCL gather", file=sys.stderr)
+            gather_mode = "nccl"
+        ok = torch.tensor([1 if R_view is not None or rank == 0 else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            gather_mode = "nccl"
     rws_bytes = hs.relight_workspace_bytes(F, kf, B)
     rws = torch.empty(rws_bytes + 1024, dtype=torch.uint8, device=dev) if rws_bytes else None
     if rws is not None:
@@ -272,6 +288,11 @@ def run_ours(args, cfg):
             launches["n"] += hs.last_launch_count()
         if world > 1:
             hsdist.broadcast_band(shifted)
+            if gather_mode == "p2p":
+                hsdist.relight_into_peer(T, shifted, V, relight_fn, R_view)
+                stream.synchronize()
+                dist.barrier()              # every rank's rows are in rank 0's buffer
+                return R_full
             _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
             return full
         relight_fn(T, shifted_band if args.start_level is not None else shifted, R)
@@ -384,7 +405,8 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": V / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(cfg, world),
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {**workload_config(cfg, world), "gather": gather_mode},
             "vertex_frames_per_sec": V * B / (ms_max * 1e-3),
             "shift_coeffs_per_sec": B * F * N * N / (ms_max * 1e-3),
             "roofline": {"bound": "hbm", "kernel": "relight_vertices", "achieved": achieved, "peak": peak,

@@ -259,6 +259,13 @@ HS_API hs_status haar_rotate_coeffs(const float* in, float* out, int log2n, int 
 
 HS_API size_t haar_rotate_workspace_bytes(int log2n, int batch);
 
+/* hs_enable_peer_access -- let kernels launched on the current device load / store the memory of
+ * `peer_device` directly (NVLink / NVSwitch), e.g. relight_vertices writing its radiance rows into
+ * rank 0's buffer opened through CUDA IPC (the fused relight + gather of SURVEY.md §8(e),
+ * DESIGN.md §6).  HS_OK if enabled or already enabled (or peer_device is the current device),
+ * HS_ERR_UNSUPPORTED if the devices cannot access each other.                                     */
+HS_API hs_status hs_enable_peer_access(int peer_device);
+
 /* ---------------------------------------------------------------------------------------------
  * hs_fill_transfer -- seeded synthetic transfer rows, generated in place (input generator, not
  * part of the method; bit-identical to synth.transfer_rows):

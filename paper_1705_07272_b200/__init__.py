@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     haar_shift_coeffs,
     haar_shift_coeffs_coarse,
     haar_shift_workspace_bytes,
+    enable_peer_access,
     hs_fill_sparse_transfer,
     hs_fill_transfer,
     last_launch_count,
@@ -46,5 +47,5 @@ __all__ = [
     "last_launch_count", "relight_shifted_workspace_bytes", "relight_vertices", "relight_workspace_bytes", "relight_vertices_shifted",
     "shift_and_relight", "hs_fill_sparse_transfer", "relight_vertices_sparse",
     "relight_sparse_workspace_bytes", "haar_pack_qtree", "relight_triple_workspace_bytes", "relight_vertices_triple",
-    "haar_rotate_coeffs", "haar_rotate_workspace_bytes",
+    "haar_rotate_coeffs", "haar_rotate_workspace_bytes", "enable_peer_access",
 ]

@@ -40,6 +40,7 @@ SIGNATURES = {
     "haar_rotate_coeffs": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p,
                                       _c.c_size_t, _c.c_void_p]),
     "haar_rotate_workspace_bytes": (_c.c_size_t, [_c.c_int, _c.c_int]),
+    "hs_enable_peer_access": (_c.c_int, [_c.c_int]),
     "hs_last_launch_count": (_c.c_int, []),
     "hs_status_string": (_c.c_char_p, [_c.c_int]),
     "hs_last_cuda_error": (_c.c_char_p, []),

@@ -28,6 +28,11 @@ def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+def enable_peer_access(peer_device: int) -> None:
+    """Allow kernels on the current device to access `peer_device`'s memory (include/haarshift.h)."""
+    check("hs_enable_peer_access", load().hs_enable_peer_access(int(peer_device)))
+
+
 def last_launch_count() -> int:
     """Kernel launches enqueued by the most recent C-ABI call on this thread."""
     return int(load().hs_last_launch_count())

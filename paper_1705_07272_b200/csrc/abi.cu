@@ -254,6 +254,40 @@ hs_status relight_vertices_sparse(const int32_t* indices, const float* values, i
   return s;
 }
 
+hs_status hs_enable_peer_access(int peer_device) {
+  g_last_launches = 0;
+  g_launches = 0;
+  int dev = 0, n = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    set_cuda_error(e, "cudaGetDevice");
+    return HS_ERR_CUDA;
+  }
+  if (peer_device < 0 || peer_device >= n) return HS_ERR_INVALID_ARG;
+  if (peer_device == dev) return HS_OK;
+  int can = 0;
+  e = cudaDeviceCanAccessPeer(&can, dev, peer_device);
+  if (e != cudaSuccess) {
+    set_cuda_error(e, "cudaDeviceCanAccessPeer");
+    return HS_ERR_CUDA;
+  }
+  if (!can) {
+    snprintf(g_err, sizeof(g_err), "device %d cannot access device %d", dev, peer_device);
+    return HS_ERR_UNSUPPORTED;
+  }
+  e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return HS_OK;
+  }
+  if (e != cudaSuccess) {
+    set_cuda_error(e, "cudaDeviceEnablePeerAccess");
+    return HS_ERR_CUDA;
+  }
+  return HS_OK;
+}
+
 size_t haar_rotate_workspace_bytes(int log2n, int batch) {
   if (log2n < 1 || log2n > 11 || batch < 1) return 0;
   return rotate_workspace_bytes_impl(log2n, batch);

@@ -7,8 +7,13 @@ One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
   row id, so every shard is bitwise the 1-GPU matrix's slice and never moves;
 * the shifted lighting band is computed once (rank 0, ``haar_shift_coeffs``) and broadcast
   (``dist.broadcast`` over NVLink) -- the one exchange step into the relight;
-* radiance is gathered to rank 0 chunk by chunk: chunk i is gathered on the NCCL stream while
-  chunk i+1 is relit (``relight_and_gather``), so the gather overlaps the HBM-bound relight.
+* radiance reaches rank 0 in one of two ways:
+  - fused (``open_peer_view`` + ``relight_into_peer``, the default of bench.py): rank 0's radiance
+    buffer is opened in every rank through CUDA IPC and each rank's relight kernel stores its
+    rows straight into it over NVLink / NVSwitch from the epilogue -- the gather IS the relight's
+    output write, no separate collective, no staging copy;
+  - NCCL (``relight_and_gather``, the baseline and the fallback): chunk i is gathered on the NCCL
+    stream while chunk i+1 is relit, so the gather overlaps the HBM-bound relight.
 
 Per-row results do not depend on the sharding (each row's reduction order is fixed inside the
 kernels), so the gathered R equals the 1-GPU R bit for bit.
@@ -109,3 +114,42 @@ def relight_and_gather(transfer_local: torch.Tensor, band: torch.Tensor, total_r
                 if hi > lo:
                     radiance_full[rs + lo:rs + hi].copy_(recv_l[r][: hi - lo])
     return local, radiance_full
+
+
+def open_peer_view(radiance_full: Optional[torch.Tensor], shape, device: torch.device, group=None) -> torch.Tensor:
+    """Every rank gets a tensor aliasing rank 0's ``radiance_full`` (CUDA IPC through torch's own
+    storage sharing; peer access to rank 0's device is enabled first).  Rank 0 passes its buffer,
+    the others pass None.  Raises if the devices cannot reach each other (callers fall back to
+    ``relight_and_gather``)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    from . import api
+    rank = dist.get_rank(group)
+    obj = [None]
+    if rank == 0:
+        fn, args = reduce_tensor(radiance_full)
+        obj = [(fn, args, radiance_full.device.index)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if rank == 0:
+        return radiance_full
+    fn, args, dev0 = obj[0]
+    api.enable_peer_access(dev0)
+    view = fn(*args)
+    if tuple(view.shape) != tuple(shape):
+        raise RuntimeError("peer view has the wrong shape")
+    return view
+
+
+def relight_into_peer(transfer_local: torch.Tensor, band: torch.Tensor, total_rows: int,
+                      relight_fn: Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None],
+                      radiance_view: torch.Tensor, group=None) -> None:
+    """The fused relight + gather: this rank's rows are written by the relight kernel directly at
+    their global offset of rank 0's radiance (``radiance_view`` from ``open_peer_view``).  The
+    caller orders completion (stream synchronise + barrier) before rank 0 reads the buffer."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    start, count = shard_rows(total_rows, world, rank)
+    if transfer_local.shape[0] != count:
+        raise ValueError(f"rank {rank}: expected {count} transfer rows, got {transfer_local.shape[0]}")
+    if count:
+        relight_fn(transfer_local, band, radiance_view[start:start + count])
