@@ -117,16 +117,11 @@ struct Geo {
   static constexpr int PADR = 2 * RS + 4;          // wrapped rows appended to the field plane
   static constexpr int HP = N / 2;                 // half-row length (parity split)
   static constexpr int PLANE = (N + PADR) * HP;    // one parity plane, padded
-  static constexpr int SMEM = (2 * PLANE + G * G + (G / 2) * (G / 2) + 64) * 4;
+  static constexpr int SCR = 2 * G * G + (G / 2) * (G / 2) + 64;   // one vertex group: S1, S2, red, T block
+  static constexpr int smem(int vg) { return (2 * PLANE + vg * SCR) * 4; }
   static_assert(kThreads % G == 0 && G % NS == 0, "geometry");
-  // transfer values a thread dots at bottom-up level lev (cells tid, tid + 256, ...)
+  // cells a thread handles at bottom-up level lev (tid, tid + 256, ...)
   static constexpr int cpt(int lev) { return (1 << (2 * lev)) > kThreads ? (1 << (2 * lev)) / kThreads : 1; }
-  static constexpr int tb_off(int lev) {
-    int o = 0;
-    for (int l = 0; l < lev; ++l) o += cpt(l);
-    return o;
-  }
-  static constexpr int NTB = tb_off(LOG2N - 1);  // levels 0 .. n-2
 };
 
 // Per-vertex shift classification, once per call (fp64, the same split as the host path).
@@ -140,106 +135,172 @@ __global__ void vertex_params_kernel(const float* __restrict__ shifts, long long
   out[v] = make_int4(qy, qx, __float_as_int((float)py), __float_as_int((float)px));
 }
 
+// Named barrier of one vertex group (256 threads; ids 1.. -- id 0 is __syncthreads).
+__device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kThreads) : "memory"); }
+
 // One bottom-up level LEV (and, recursively, all coarser ones): shifted fields of level LEV from
-// level LEV+1 (periodic), the detail output dotted with the prefetched transfer values tb.
-template <int LOG2N, int FLD, int LEV, int NTB>
-__device__ __forceinline__ void bottom_up(const float* src, float* dst, const float (&tb)[NTB], float& acc) {
+// level LEV+1 (periodic), the detail output dotted with T_v's coefficients of type FLD.  Levels
+// with more than 64 cells use the whole vertex group (named barrier between levels); the last
+// levels (<= 64 cells) run on warp 0 alone (warp-synchronous), the other warps go on.
+constexpr int kWarpLevel = 3;
+template <int LEV>
+struct BU {   // cells per thread of bottom-up level LEV and the offset of its prefetched T values
+  static constexpr bool WARP = LEV <= kWarpLevel;
+  static constexpr int STRIDE = WARP ? 32 : kThreads;
+  static constexpr int CPT = ((1 << (2 * LEV)) + STRIDE - 1) / STRIDE;
+  static constexpr int OFF = LEV == 0 ? 0 : BU<(LEV > 0 ? LEV - 1 : 0)>::OFF + BU<(LEV > 0 ? LEV - 1 : 0)>::CPT;
+};
+template <>
+struct BU<0> {
+  static constexpr bool WARP = true;
+  static constexpr int STRIDE = 32;
+  static constexpr int CPT = 1;
+  static constexpr int OFF = 0;
+};
+
+// T_v's coefficients of type FLD at levels 0 .. TOP that this thread dots, loaded ahead of use
+template <int FLD, int LEV, int NT>
+__device__ __forceinline__ void prefetch_t(const float* __restrict__ Tv, int tid, float (&tp)[NT]) {
   if constexpr (LEV >= 0) {
-    using Gm = Geo<LOG2N>;
-    constexpr int g = 1 << LEV, Gs = 2 * g;
-    const float osc = pow2f(-LEV);
-    const int tid = threadIdx.x;
+    using B = BU<LEV>;
+    const float* Tl = Tv + ((long long)(1 + FLD) << (2 * LEV));
 #pragma unroll
-    for (int k = 0; k < Gm::cpt(LEV); ++k) {
-      const int idx = tid + k * kThreads;
-      if (idx < g * g) {
-        const int i = idx >> LEV, jj = idx & (g - 1);
-        const float* p0 = src + (2 * i) * Gs;
-        const float* p1 = p0 + Gs;
-        const float* p2 = src + ((2 * i + 2) & (Gs - 1)) * Gs;
-        const int c0 = 2 * jj, c1 = 2 * jj + 1, c2 = (2 * jj + 2) & (Gs - 1);
-        float fv, dv;
-        if (FLD == 0) {
-          fv = 0.25f * (p0[c0] + 2.f * p0[c1] + p0[c2] + p1[c0] + 2.f * p1[c1] + p1[c2]);
-          dv = 0.25f * (p0[c0] + p1[c0]);
-        } else if (FLD == 1) {
-          fv = 0.25f * (p0[c0] + 2.f * p1[c0] + p2[c0] + p0[c1] + 2.f * p1[c1] + p2[c1]);
-          dv = 0.25f * (p0[c0] + p0[c1]);
-        } else {
-          fv = 0.25f * ((p0[c0] + 2.f * p0[c1] + p0[c2]) + 2.f * (p1[c0] + 2.f * p1[c1] + p1[c2]) +
-                        (p2[c0] + 2.f * p2[c1] + p2[c2]));
-          dv = 0.25f * p0[c0];
-        }
-        dst[idx] = fv;
-        acc = fmaf(dv * osc, tb[Gm::tb_off(LEV) + k], acc);
-      }
+    for (int k = 0; k < B::CPT; ++k) {
+      const int idx = tid + k * B::STRIDE;
+      tp[B::OFF + k] = ((!B::WARP || tid < 32) && idx < (1 << (2 * LEV))) ? __ldg(Tl + idx) : 0.f;
     }
-    __syncthreads();
-    bottom_up<LOG2N, FLD, LEV - 1, NTB>(dst, const_cast<float*>(src), tb, acc);
+    prefetch_t<FLD, LEV - 1, NT>(Tv, tid, tp);
   }
 }
 
-// One (face f, field FLD) unit over the vertex range [v0, v1).  FLD: 0 = X -> H, 1 = Y -> V,
-// 2 = Z -> D.  The field plane sits in shared memory parity split and padded with PADR wrapped
-// rows, so every tap of a thread's strip is an immediate offset from four per-vertex bases.
-template <int LOG2N, int FLD>
-__device__ __forceinline__ void unit_body(float* sm, const float* __restrict__ T, int faces, int f,
-                                          const int4* __restrict__ vparams, float* __restrict__ partial, int unit,
-                                          int units, long long v0, long long v1) {
+template <int LOG2N, int FLD, int LEV, int NT>
+__device__ __forceinline__ void bottom_up(const float* src, float* dst, const float (&tp)[NT], int tid, int bar,
+                                          float& acc) {
+  if constexpr (LEV >= 0) {
+    constexpr int g = 1 << LEV, Gs = 2 * g;
+    constexpr bool WARP = BU<LEV>::WARP;
+    constexpr int STRIDE = BU<LEV>::STRIDE;
+    constexpr int CPT = BU<LEV>::CPT;
+    const float osc = pow2f(-LEV);
+    if (!WARP || tid < 32) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int idx = tid + k * STRIDE;
+        if (idx < g * g) {
+          const float t = tp[BU<LEV>::OFF + k];
+          const int i = idx >> LEV, jj = idx & (g - 1);
+          const float* p0 = src + (2 * i) * Gs;
+          const float* p1 = p0 + Gs;
+          const float* p2 = src + ((2 * i + 2) & (Gs - 1)) * Gs;
+          const int c0 = 2 * jj, c1 = 2 * jj + 1, c2 = (2 * jj + 2) & (Gs - 1);
+          float fv, dv;
+          if (FLD == 0) {
+            fv = 0.25f * (p0[c0] + 2.f * p0[c1] + p0[c2] + p1[c0] + 2.f * p1[c1] + p1[c2]);
+            dv = 0.25f * (p0[c0] + p1[c0]);
+          } else if (FLD == 1) {
+            fv = 0.25f * (p0[c0] + 2.f * p1[c0] + p2[c0] + p0[c1] + 2.f * p1[c1] + p2[c1]);
+            dv = 0.25f * (p0[c0] + p0[c1]);
+          } else {
+            fv = 0.25f * ((p0[c0] + 2.f * p0[c1] + p0[c2]) + 2.f * (p1[c0] + 2.f * p1[c1] + p1[c2]) +
+                          (p2[c0] + 2.f * p2[c1] + p2[c2]));
+            dv = 0.25f * p0[c0];
+          }
+          if (LEV > 0) dst[idx] = fv;
+          acc = fmaf(dv * osc, t, acc);
+        }
+      }
+    }
+    if constexpr (LEV > 0) {
+      if constexpr (LEV - 1 <= kWarpLevel) {
+        if constexpr (WARP) __syncwarp();
+        else group_sync(bar);   // level LEV complete before warp 0 reads it
+      } else {
+        group_sync(bar);
+      }
+      bottom_up<LOG2N, FLD, LEV - 1, NT>(dst, const_cast<float*>(src), tp, tid, bar, acc);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init1(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)));
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(smem_addr(b)),
+      "r"(ph)
+      : "memory");
+}
+// one 1D bulk copy global -> shared completing on the group's mbarrier
+__device__ __forceinline__ void bulk_to_smem(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
+}
+
+// One (face f, field FLD) unit: vertex group `grp` (256 threads) of the CTA processes vertices
+// v0 + grp, v0 + grp + VG, ... < v1.  FLD: 0 = X -> H, 1 = Y -> V, 2 = Z -> D.  The field plane
+// (shared by the VG groups) sits in shared memory parity split and padded with PADR wrapped rows,
+// so every tap of a thread's strip is an immediate offset from four per-vertex bases; each group
+// has its own level n-1 / n-2 scratch and synchronises on its own named barrier.
+template <int LOG2N, int FLD, int VG>
+__device__ __forceinline__ void unit_body(const float* plane, float* scratch, uint64_t* mbars, const float* __restrict__ T,
+                                          int faces, int f, const int4* __restrict__ vparams, float* __restrict__ partial,
+                                          int unit, int units, long long v0, long long v1) {
   using Gm = Geo<LOG2N>;
   constexpr int N = Gm::N, G = Gm::G, RS = Gm::RS, HP = Gm::HP, PLANE = Gm::PLANE;
   constexpr int n = LOG2N;
   constexpr int NTAP = (FLD == 1) ? 3 : 4;
-  float* S1 = sm + 2 * PLANE;       // shifted field at level n-1 (G x G)
-  float* S2 = S1 + G * G;           // level n-2
+  const int grp = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
+  const int bar = 1 + grp;
+  float* S1 = scratch + grp * Gm::SCR;   // shifted field at level n-1 (G x G)
+  float* S2 = S1 + G * G;                // level n-2
   float* red = S2 + (G / 2) * (G / 2);
+  float* Tb = red + 64;                  // T_v's level n-1 block of type FLD (G x G), bulk-copied
+  uint64_t* mb = mbars + grp;
   const long long NN = (long long)N * N;
   const long long Kt = (long long)faces * NN;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int j = tid % G;            // level n-1 column owned by this thread
   const int i0 = (tid / G) * RS;    // first output row of this thread's strip
   constexpr int lvl1 = n - 1;
+  constexpr uint32_t TB_BYTES = G * G * 4;
   const float osc1 = pow2f(-lvl1);
+  auto tblock = [&](long long vv) { return T + vv * Kt + (long long)f * NN + ((long long)(1 + FLD) << (2 * lvl1)); };
 
-#define HS_LOAD_T(VV, TV, TB, PR)                                                        \
-  if ((VV) < v1) {                                                                      \
-    PR = __ldg(vparams + (VV));                                                         \
-    const float* Tv_ = T + (VV) * Kt + (long long)f * NN;                               \
-    const float* Trow_ = Tv_ + ((long long)(1 + FLD) << (2 * lvl1)) + j;                \
-    _Pragma("unroll") for (int r_ = 0; r_ < RS; ++r_) TV[r_] = __ldg(Trow_ + (i0 + r_) * G); \
-    _Pragma("unroll") for (int lev_ = 0; lev_ <= n - 2; ++lev_) {                       \
-      const float* Tl_ = Tv_ + ((long long)(1 + FLD) << (2 * lev_));                    \
-      _Pragma("unroll") for (int k_ = 0; k_ < Gm::cpt(lev_); ++k_) {                    \
-        const int idx_ = tid + k_ * kThreads;                                           \
-        TB[Gm::tb_off(lev_) + k_] = (idx_ < (1 << (2 * lev_))) ? __ldg(Tl_ + idx_) : 0.f; \
-      }                                                                                 \
-    }                                                                                   \
-  }
-  constexpr int NTBX = Gm::NTB > 0 ? Gm::NTB : 1;
-  float tv[RS], tb[NTBX];
-  int4 pr = make_int4(0, 0, 0, 0);
-  HS_LOAD_T(v0, tv, tb, pr);
-  for (long long v = v0; v < v1; ++v) {
-    float tvn[RS], tbn[NTBX];
-    int4 prn = pr;
-    HS_LOAD_T(v + 1, tvn, tbn, prn);  // software pipeline: next vertex's loads in flight
+  if (tid == 0 && v0 + grp < v1) bulk_to_smem(Tb, tblock(v0 + grp), TB_BYTES, mb);
+  uint32_t phase = 0;
+  for (long long v = v0 + grp; v < v1; v += VG) {
+    const int4 pr = __ldg(vparams + v);
+    const float* Tv = T + v * Kt + (long long)f * NN;
     const int qy = pr.x, qx = pr.y;
     const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
     float acc = 0.f;
+    constexpr int NT = BU<LOG2N - 2>::OFF + BU<LOG2N - 2>::CPT;
+    float tp[NT];
+    prefetch_t<FLD, LOG2N - 2, NT>(Tv, tid, tp);   // in flight during the fused stencil
     // ---- level n -> n-1: fused shift + first bottom-up, sliding down this thread's rows.
-    // window row u (0-based) = level-n row ((2 i0 - qy - 1) & (N-1)) + u, no wrap (padded plane);
+    // window row u = level-n row ((2 i0 - qy - 1) & (N-1)) + u (padded plane, no wrap);
     // column tap v = -1..2 at level n: c = 2j - qx + v (periodic), parity split
     const int rs = (2 * i0 - qy - 1) & (N - 1);
     const float* base[NTAP];
 #pragma unroll
     for (int vv = 0; vv < NTAP; ++vv) {
       const int c = (2 * j - qx + vv - 1) & (N - 1);
-      base[vv] = sm + (c & 1) * PLANE + rs * HP + (c >> 1);
+      base[vv] = plane + (c & 1) * PLANE + rs * HP + (c >> 1);
     }
-    // horizontal filters: field tent [w1, w0+2w1, 2w0+w1, w0] (X, Z) or [w1, 1, w0] (Y);
-    // detail [w1, w0] (X, Z) or the Y field filter itself
     const float ta = wx1, tb0 = wx0 + 2.f * wx1, tb1 = 2.f * wx0 + wx1, tc = wx0;
-    float hA[RS * 2 + 2], hB[RS * 2 + 2];
+    const float ua = wy1, ub0 = wy0 + 2.f * wy1, ub1 = 2.f * wy0 + wy1, uc = wy0;
+    mbar_wait_parity(mb, phase);   // T_v's level n-1 block has landed
+    phase ^= 1;
+    // horizontal filters of window row u, streamed: output row r needs rows 2r .. 2r+2 (X) or
+    // 2r .. 2r+3 (Y, Z) and is emitted as soon as its last row is filtered
+    float hA[2 * RS + 2], hB[2 * RS + 2];
 #pragma unroll
     for (int u = 0; u < 2 * RS + 2; ++u) {
       const float x_1 = base[0][u * HP], x0 = base[1][u * HP], x1 = base[2][u * HP];
@@ -251,51 +312,47 @@ __device__ __forceinline__ void unit_body(float* sm, const float* __restrict__ T
         hA[u] = fmaf(ta, x_1, fmaf(tb0, x0, fmaf(tb1, x1, tc * x2)));
         hB[u] = fmaf(wx1, x_1, wx0 * x0);
       }
-    }
-    const float ua = wy1, ub0 = wy0 + 2.f * wy1, ub1 = 2.f * wy0 + wy1, uc = wy0;
-#pragma unroll
-    for (int r = 0; r < RS; ++r) {
-      const int u = 2 * r;  // window rows u .. u+3 <-> taps -1..2 of output row i0 + r
-      float fld, det;
-      if (FLD == 0) {  // X: rows [w1, 1, w0] on taps -1..1, detail rows the same
-        fld = 0.25f * fmaf(wy1, hA[u], fmaf(wy0, hA[u + 2], hA[u + 1]));
-        det = 0.25f * fmaf(wy1, hB[u], fmaf(wy0, hB[u + 2], hB[u + 1]));
-      } else {         // Y, Z: rows tent on taps -1..2; detail rows [w1, w0] on taps -1, 0
-        fld = 0.25f * fmaf(ua, hA[u], fmaf(ub0, hA[u + 1], fmaf(ub1, hA[u + 2], uc * hA[u + 3])));
-        det = 0.25f * fmaf(wy1, hB[u], wy0 * hB[u + 1]);
+      constexpr int LAST = (FLD == 0) ? 2 : 3;
+      if (u >= LAST && ((u - LAST) & 1) == 0) {
+        const int r = (u - LAST) >> 1;
+        const int w = 2 * r;
+        float fl, det;
+        if (FLD == 0) {  // X: rows [w1, 1, w0] on taps -1..1, detail rows the same
+          fl = 0.25f * fmaf(wy1, hA[w], fmaf(wy0, hA[w + 2], hA[w + 1]));
+          det = 0.25f * fmaf(wy1, hB[w], fmaf(wy0, hB[w + 2], hB[w + 1]));
+        } else {         // Y, Z: rows tent on taps -1..2; detail rows [w1, w0] on taps -1, 0
+          fl = 0.25f * fmaf(ua, hA[w], fmaf(ub0, hA[w + 1], fmaf(ub1, hA[w + 2], uc * hA[w + 3])));
+          det = 0.25f * fmaf(wy1, hB[w], wy0 * hB[w + 1]);
+        }
+        S1[(i0 + r) * G + j] = fl;
+        acc = fmaf(det * osc1, Tb[(i0 + r) * G + j], acc);
       }
-      S1[(i0 + r) * G + j] = fld;
-      acc = fmaf(det * osc1, tv[r], acc);
     }
-    __syncthreads();
+    group_sync(bar);
+    // Tb is free: the next vertex's block streams in during the bottom-up
+    if (tid == 0 && v + VG < v1) bulk_to_smem(Tb, tblock(v + VG), TB_BYTES, mb);
     // ---- bottom-up n-2 .. 0 (periodic), ping-pong S1 -> S2 -> S1 ... (compile-time levels)
-    bottom_up<LOG2N, FLD, LOG2N - 2>(S1, S2, tb, acc);
-    // ---- CTA reduction of the partial sum (fixed order -> deterministic)
+    bottom_up<LOG2N, FLD, LOG2N - 2, NT>(S1, S2, tp, tid, bar, acc);
+    // ---- group reduction of the partial sum (fixed order -> deterministic)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) red[warp] = acc;
-    __syncthreads();
+    group_sync(bar);
     if (tid == 0) {
-      float s = 0.f;
+      float sum = 0.f;
 #pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-      partial[v * units + unit] = s;
+      for (int w = 0; w < kThreads / 32; ++w) sum += red[w];
+      partial[v * units + unit] = sum;
     }
-#pragma unroll
-    for (int r = 0; r < RS; ++r) tv[r] = tvn[r];
-#pragma unroll
-    for (int k = 0; k < Gm::NTB; ++k) tb[k] = tbn[k];
-    pr = prn;
   }
-#undef HS_LOAD_T
 }
 
-template <int LOG2N>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int LOG2N, int VG>
+__global__ void __launch_bounds__(kThreads * VG, 1)
     relight_shifted_unit_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ fields,
                                 const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
   using Gm = Geo<LOG2N>;
-  constexpr int N = Gm::N, HP = Gm::HP, PLANE = Gm::PLANE, PADR = Gm::PADR;
+  constexpr int N = Gm::N, HP = Gm::HP, PLANE = Gm::PLANE;
   extern __shared__ __align__(16) float sm[];
   const int units = 3 * faces;
   const int unit = blockIdx.x % units;
@@ -305,17 +362,21 @@ __global__ void __launch_bounds__(kThreads, 2)
   // field plane -> smem, parity split [2][N + PADR][N/2], rows N.. = rows 0.. (periodic padding)
   {
     const float* src = fields + ((long long)f * 3 + t) * NN;
-    for (int idx = threadIdx.x; idx < 2 * (N + PADR) * HP; idx += kThreads) {
+    for (int idx = threadIdx.x; idx < 2 * PLANE; idx += blockDim.x) {
       const int par = idx / PLANE, rem = idx - par * PLANE;
       const int r = rem / HP, c = rem - r * HP;
       sm[idx] = __ldg(src + (long long)par * (NN / 2) + (r & (N - 1)) * HP + c);
     }
   }
+  __shared__ __align__(8) uint64_t mbars[VG];
+  if (threadIdx.x < VG) mbar_init1(&mbars[threadIdx.x]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
-  if (t == 0) unit_body<LOG2N, 0>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
-  else if (t == 1) unit_body<LOG2N, 1>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
-  else unit_body<LOG2N, 2>(sm, T, faces, f, vparams, partial, unit, units, v0, v1);
+  float* scratch = sm + 2 * PLANE;
+  if (t == 0) unit_body<LOG2N, 0, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else if (t == 1) unit_body<LOG2N, 1, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else unit_body<LOG2N, 2, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
 }
 
 __global__ void relight_shifted_finish_kernel(const float* __restrict__ partial, const float* __restrict__ T,
@@ -342,25 +403,26 @@ int num_sms_rs() {
   return n;
 }
 
+constexpr int kVG = 3;   // vertex groups per CTA sharing one field plane (1 CTA per SM)
+
 template <int LOG2N>
 hs_status launch_unit(const float* T, long long V, int faces, const float* fields, const int4* shifts,
                       float* partial, cudaStream_t st) {
+  constexpr int SM = Geo<LOG2N>::smem(kVG);
+  static_assert(SM <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
-    HS_CHECK_CUDA(cudaFuncSetAttribute(relight_shifted_unit_kernel<LOG2N>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<LOG2N>::SMEM),
+    HS_CHECK_CUDA(cudaFuncSetAttribute(relight_shifted_unit_kernel<LOG2N, kVG>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SM),
                   "cudaFuncSetAttribute(relight_shifted_unit_kernel)");
     attr = true;
   }
   const int units = 3 * faces;
-  int per_sm = 227 * 1024 / (Geo<LOG2N>::SMEM + 1024);
-  if (per_sm > 2) per_sm = 2;
-  if (per_sm < 1) per_sm = 1;
-  int nsplit = (num_sms_rs() * per_sm) / units;
+  int nsplit = num_sms_rs() / units;   // one CTA per SM
   if (nsplit < 1) nsplit = 1;
   if (nsplit > V) nsplit = (int)V;
-  relight_shifted_unit_kernel<LOG2N><<<units * nsplit, kThreads, Geo<LOG2N>::SMEM, st>>>(T, V, faces, fields, shifts,
-                                                                                           partial, nsplit);
+  relight_shifted_unit_kernel<LOG2N, kVG><<<units * nsplit, kThreads * kVG, SM, st>>>(T, V, faces, fields, shifts,
+                                                                                      partial, nsplit);
   HS_CHECK_LAUNCH("relight_shifted_unit_kernel");
   return HS_OK;
 }
