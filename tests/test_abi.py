@@ -111,6 +111,42 @@ def test_relight_validation_before_device(lib):
     assert h(FAKE, 0, 1, 6, 12, 1, 2, None) == 1
 
 
+def test_widened_entries_validate_before_device(lib):
+    """rows f1-f4 and the multi-GPU helper reject bad arguments with a status before any device
+    access (so these run without a GPU)."""
+    W = FAKE * 16
+    t = lib.relight_vertices_triple
+    need = lib.relight_triple_workspace_bytes(100, 6, 1024, 64)
+    assert need >= 64 * 6144 * 4 and lib.relight_triple_workspace_bytes(100, 6, 16, 64) == 0   # k_face < 64
+    assert t(None, FAKE, 100, 6, 1024, FAKE * 2, 1024, 64, FAKE * 4, W, need, None) == 1         # null brdf
+    assert t(FAKE, FAKE * 2, 100, 6, 16, FAKE * 3, 16, 64, FAKE * 4, W, need, None) == 1         # k_face < 64
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 512, 64, FAKE * 4, W, need, None) == 1      # stride < k
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 1024, 64, FAKE * 4, W, need - 1, None) == 1  # small ws
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 1024, 64, FAKE * 4, W + 512, need, None) == 2  # ws align
+    pk = lib.haar_pack_qtree
+    assert pk(FAKE, 4, 6, 64, 2, FAKE * 4, None) == 1                                           # log2k < 3
+    assert pk(FAKE, 4, 6, 32, 3, FAKE * 4, None) == 1                                           # stride < 4^k
+    assert pk(FAKE, 4, 6, 64, 3, FAKE + 64, None) == 1                                          # overlap
+    r = lib.haar_rotate_coeffs
+    ang = np.zeros(8)
+    ap = ang.ctypes.data_as(ctypes.c_void_p)
+    rneed = lib.haar_rotate_workspace_bytes(5, 4)
+    assert rneed > 0 and lib.haar_rotate_workspace_bytes(12, 4) == 0
+    assert r(FAKE, FAKE * 4, 12, 4, ap, W, rneed, None) == 1                                    # log2n
+    assert r(FAKE, FAKE * 4, 5, 4, ap, W, rneed - 1, None) == 1                                 # small ws
+    ang[3] = np.nan
+    assert r(FAKE, FAKE * 4, 5, 4, ap, W, rneed, None) == 1                                     # non-finite
+    ang[3] = 0.0
+    assert r(FAKE, FAKE + 64, 5, 4, ap, W, rneed, None) == 1                                    # overlap
+    sp = lib.relight_vertices_sparse
+    assert sp(FAKE, FAKE * 2, 10, 8, FAKE * 3, 1 << 31, 64, FAKE * 4, W, 1 << 30, None) == 1    # C >= 2^31
+    assert sp(FAKE, FAKE * 2, 10, 8, FAKE * 3, 1000, 1025, FAKE * 4, W, 1 << 30, None) == 1     # batch
+    c = lib.haar_shift_coeffs_coarse
+    assert c(FAKE, FAKE * 4, 8, 9, 6, 1, ap, 5, W, 1 << 30, None) == 1                          # L > n
+    assert c(FAKE, FAKE * 4, 8, 5, 6, 1, ap, 6, W, 1 << 30, None) == 1                          # band > L
+    assert lib.hs_enable_peer_access(-1) in (1, 4)
+
+
 def test_no_device_fails_loudly(lib):
     """Valid arguments on a host without a usable sm_100 device: an error status, never a silent
     CPU computation."""
