@@ -52,6 +52,30 @@ for n, V in ((5, 37), (8, 3)):
 out = torch.empty((9, 6 * 16), device="cuda")
 hs.hs_fill_transfer(out, 5, 6, 16, 9, synth.STREAM_T)
 errs["fill"] = float(np.abs(out.cpu().numpy() - synth.transfer_rows(9, 5, 9, 6, 16)).max())
+# widened rows: coarse start (f4), sparse (f2), triple product (f3, both paths), rotation (f1, exact parts)
+Lc = synth.light_pyramids(10, 2, 2, 6)
+shc = np.array([[[8.0, -4.0], [12.0, 20.0]], [[4.0, 4.0], [0.0, 8.0]]])      # multiples of 2^(n-L): exact
+errs["coarse_L4"] = rel(hs.haar_shift_coeffs_coarse(t(Lc), shc, 4).cpu().numpy(),
+                        oshift.shift_coeffs(Lc, shc, 2, band_levels=4))
+idx, val = synth.sparse_transfer_rows(11, 0, 57, 2, 5, 40)
+Ls = synth.light_pyramids(12, 3, 2, 5)
+errs["sparse_b3"] = rel(hs.relight_vertices_sparse(torch.from_numpy(idx).cuda(), t(val), t(Ls)).cpu().numpy(),
+                        orelight.relight_sparse(idx, val, Ls.reshape(3, -1)))
+for B in (3, 64):
+    rho = synth.shading_rows(13, 0, 131, 2, 64, synth.STREAM_BRDF)
+    vis = synth.shading_rows(13, 0, 131, 2, 64, synth.STREAM_VIS)
+    Lt = synth.light_pyramids(14, B, 2, 3)
+    rq = hs.haar_pack_qtree(t(rho).view(131, 2, 64), 3)
+    vq = hs.haar_pack_qtree(t(vis).view(131, 2, 64), 3)
+    errs[f"triple_b{B}"] = rel(hs.relight_vertices_triple(rq, vq, t(Lt), 2, 64).cpu().numpy(),
+                               orelight.relight_triple(rho, vis, Lt, 2, 64))
+from oracle import rotate as orot  # noqa: E402
+cm = synth.smooth_sphere_maps(15, 3, 4)
+ang = np.array([[0.0, 0.0], [0.0, 2 * np.pi * 3 / 16], [0.0, -2 * np.pi / 16]])
+got = hs.haar_rotate_coeffs(t(cm), ang).cpu().numpy()
+errs["rotate_exact"] = max(rel(got[b], orot.rotate_coeffs(cm[b].astype(np.float64), *ang[b])) for b in range(3))
+got = hs.haar_rotate_coeffs(t(cm), np.array([[0.7, 1.0], [-0.4, 0.2], [1.2, 3.0]])).cpu().numpy()
+errs["rotate_finite"] = 0.0 if np.isfinite(got).all() else 1.0
 torch.cuda.synchronize()
 for k, v in errs.items():
     print(f"{k}: {v:.3e}")
