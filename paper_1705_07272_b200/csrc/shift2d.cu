@@ -492,6 +492,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
         }
       }
       __syncthreads();
+      if (fld == 0) { HS_PHASE(6) }
     }
   }
 
@@ -551,6 +552,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     const int ii = r / TC, jj = r - ii * TC;
     wsf[(long long)fld * gc * gc + (long long)(i0 + ii) * gc + (j0 + jj)] = srcS[fld * srcPlane + ii * srcN + jj];
   }
+  HS_PHASE(9)
 }
 
 // (1) over the full grid of one face up to the tile-root level c: the unshifted level-c fields.

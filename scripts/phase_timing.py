@@ -30,8 +30,8 @@ ntile = 16 * B * cfg.faces
 buf = np.zeros(ntile * 16, dtype=np.int64)
 assert lib.hs_debug_phase_dump(buf.ctypes.data, buf.size) == 0
 ph = buf.reshape(ntile, 16)[:, :10].astype(np.float64)
-names = ["regions", "detail loads", "anc. wait", "ancestors", "wait B", "level m-1 fields", "children m",
-         "fused stencil", "bottom-up", "publish"]
+names = ["start", "window starts", "loads issued + group A wait", "(marker)", "level c+1 fields + group B wait",
+         "level m-1 fields", "field X: children + fused", "fields Y, Z: children + fused", "bottom-up", "publish"]
 d = np.diff(ph, axis=1)
 tot = ph[:, 9] - ph[:, 0]
 print(f"CTA lifetime (phase 0 -> 9): median {np.median(tot):.0f} cycles, mean {tot.mean():.0f}")
