@@ -112,14 +112,18 @@ template <int LOG2N>
 struct Geo {
   static constexpr int N = 1 << LOG2N;
   static constexpr int G = N / 2;                  // level n-1 side
-  static constexpr int NS = kThreads / G;          // row strips at level n-1
+  // adjacent level n-1 columns per thread (taps shared): 2 cuts the tap loads per output by 25 % but makes
+  // the per-thread stride 2 floats (2-way bank conflicts) -- measured slower (20.0 vs 16.5 ms at c4)
+  static constexpr int CPT = 1;
+  static constexpr int TPR = G / CPT;              // threads per level n-1 row
+  static constexpr int NS = kThreads / TPR;        // row strips at level n-1
   static constexpr int RS = G / NS;                // output rows per strip
   static constexpr int PADR = 2 * RS + 4;          // wrapped rows appended to the field plane
   static constexpr int HP = N / 2;                 // half-row length (parity split)
   static constexpr int PLANE = (N + PADR) * HP;    // one parity plane, padded
   static constexpr int SCR = 2 * G * G + (G / 2) * (G / 2) + 64;   // one vertex group: S1, S2, red, T block
   static constexpr int smem(int vg) { return (2 * PLANE + vg * SCR) * 4; }
-  static_assert(kThreads % G == 0 && G % NS == 0, "geometry");
+  static_assert(kThreads % TPR == 0 && G % NS == 0, "geometry");
   // cells a thread handles at bottom-up level lev (tid, tid + 256, ...)
   static constexpr int cpt(int lev) { return (1 << (2 * lev)) > kThreads ? (1 << (2 * lev)) / kThreads : 1; }
 };
@@ -266,8 +270,9 @@ __device__ __forceinline__ void unit_body(const float* plane, float* scratch, ui
   const long long NN = (long long)N * N;
   const long long Kt = (long long)faces * NN;
   const int lane = tid & 31, warp = tid >> 5;
-  const int j = tid % G;            // level n-1 column owned by this thread
-  const int i0 = (tid / G) * RS;    // first output row of this thread's strip
+  constexpr int CPT = Gm::CPT;
+  const int j = (tid % Gm::TPR) * CPT;  // first level n-1 column owned by this thread
+  const int i0 = (tid / Gm::TPR) * RS;  // first output row of this thread's strip
   constexpr int lvl1 = n - 1;
   constexpr uint32_t TB_BYTES = G * G * 4;
   const float osc1 = pow2f(-lvl1);
@@ -286,13 +291,15 @@ __device__ __forceinline__ void unit_body(const float* plane, float* scratch, ui
     prefetch_t<FLD, LOG2N - 2, NT>(Tv, tid, tp);   // in flight during the fused stencil
     // ---- level n -> n-1: fused shift + first bottom-up, sliding down this thread's rows.
     // window row u = level-n row ((2 i0 - qy - 1) & (N-1)) + u (padded plane, no wrap);
-    // column tap v = -1..2 at level n: c = 2j - qx + v (periodic), parity split
+    // column tap k = 0 .. NTK-1 at level n: c = 2j - qx - 1 + k (periodic), parity split; output
+    // column j + e uses taps 2e .. 2e + NTAP - 1
+    constexpr int NTK = 2 * (CPT - 1) + NTAP;
     const int rs = (2 * i0 - qy - 1) & (N - 1);
-    const float* base[NTAP];
+    const float* base[NTK];
 #pragma unroll
-    for (int vv = 0; vv < NTAP; ++vv) {
-      const int c = (2 * j - qx + vv - 1) & (N - 1);
-      base[vv] = plane + (c & 1) * PLANE + rs * HP + (c >> 1);
+    for (int k = 0; k < NTK; ++k) {
+      const int c = (2 * j - qx + k - 1) & (N - 1);
+      base[k] = plane + (c & 1) * PLANE + rs * HP + (c >> 1);
     }
     const float ta = wx1, tb0 = wx0 + 2.f * wx1, tb1 = 2.f * wx0 + wx1, tc = wx0;
     const float ua = wy1, ub0 = wy0 + 2.f * wy1, ub1 = 2.f * wy0 + wy1, uc = wy0;
@@ -300,32 +307,49 @@ __device__ __forceinline__ void unit_body(const float* plane, float* scratch, ui
     phase ^= 1;
     // horizontal filters of window row u, streamed: output row r needs rows 2r .. 2r+2 (X) or
     // 2r .. 2r+3 (Y, Z) and is emitted as soon as its last row is filtered
-    float hA[2 * RS + 2], hB[2 * RS + 2];
+    float hA[CPT][2 * RS + 2], hB[CPT][2 * RS + 2];
 #pragma unroll
     for (int u = 0; u < 2 * RS + 2; ++u) {
-      const float x_1 = base[0][u * HP], x0 = base[1][u * HP], x1 = base[2][u * HP];
-      if (FLD == 1) {
-        hA[u] = fmaf(wx1, x_1, fmaf(wx0, x1, x0));
-        hB[u] = hA[u];
-      } else {
-        const float x2 = base[NTAP - 1][u * HP];
-        hA[u] = fmaf(ta, x_1, fmaf(tb0, x0, fmaf(tb1, x1, tc * x2)));
-        hB[u] = fmaf(wx1, x_1, wx0 * x0);
+      float x[NTK];
+#pragma unroll
+      for (int k = 0; k < NTK; ++k) x[k] = base[k][u * HP];
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) {
+        const float x_1 = x[2 * e], x0 = x[2 * e + 1], x1 = x[2 * e + 2];
+        if (FLD == 1) {
+          hA[e][u] = fmaf(wx1, x_1, fmaf(wx0, x1, x0));
+          hB[e][u] = hA[e][u];
+        } else {
+          const float x2 = x[2 * e + 3];
+          hA[e][u] = fmaf(ta, x_1, fmaf(tb0, x0, fmaf(tb1, x1, tc * x2)));
+          hB[e][u] = fmaf(wx1, x_1, wx0 * x0);
+        }
       }
       constexpr int LAST = (FLD == 0) ? 2 : 3;
       if (u >= LAST && ((u - LAST) & 1) == 0) {
         const int r = (u - LAST) >> 1;
         const int w = 2 * r;
-        float fl, det;
-        if (FLD == 0) {  // X: rows [w1, 1, w0] on taps -1..1, detail rows the same
-          fl = 0.25f * fmaf(wy1, hA[w], fmaf(wy0, hA[w + 2], hA[w + 1]));
-          det = 0.25f * fmaf(wy1, hB[w], fmaf(wy0, hB[w + 2], hB[w + 1]));
-        } else {         // Y, Z: rows tent on taps -1..2; detail rows [w1, w0] on taps -1, 0
-          fl = 0.25f * fmaf(ua, hA[w], fmaf(ub0, hA[w + 1], fmaf(ub1, hA[w + 2], uc * hA[w + 3])));
-          det = 0.25f * fmaf(wy1, hB[w], wy0 * hB[w + 1]);
+        float fl[CPT], det[CPT];
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) {
+          if (FLD == 0) {  // X: rows [w1, 1, w0] on taps -1..1, detail rows the same
+            fl[e] = 0.25f * fmaf(wy1, hA[e][w], fmaf(wy0, hA[e][w + 2], hA[e][w + 1]));
+            det[e] = 0.25f * fmaf(wy1, hB[e][w], fmaf(wy0, hB[e][w + 2], hB[e][w + 1]));
+          } else {         // Y, Z: rows tent on taps -1..2; detail rows [w1, w0] on taps -1, 0
+            fl[e] = 0.25f * fmaf(ua, hA[e][w], fmaf(ub0, hA[e][w + 1], fmaf(ub1, hA[e][w + 2], uc * hA[e][w + 3])));
+            det[e] = 0.25f * fmaf(wy1, hB[e][w], wy0 * hB[e][w + 1]);
+          }
         }
-        S1[(i0 + r) * G + j] = fl;
-        acc = fmaf(det * osc1, Tb[(i0 + r) * G + j], acc);
+        const int o = (i0 + r) * G + j;
+        if constexpr (CPT == 2) {
+          *reinterpret_cast<float2*>(S1 + o) = make_float2(fl[0], fl[1]);
+          const float2 tt = *reinterpret_cast<const float2*>(Tb + o);
+          acc = fmaf(det[0] * osc1, tt.x, acc);
+          acc = fmaf(det[1] * osc1, tt.y, acc);
+        } else {
+          S1[o] = fl[0];
+          acc = fmaf(det[0] * osc1, Tb[o], acc);
+        }
       }
     }
     group_sync(bar);
