@@ -178,7 +178,7 @@ def run_reference(args, cfg):
     times = []
     sampler = oracle_sample_triple if cfg.name == "c5t" else oracle_sample
     for i in range(warm + steps):
-        full, desc = sampler(cfg, 1, 2000, seed_off=i * 2000)
+        full, desc = sampler(cfg, 1, 20000, seed_off=i * 20000)
         if i >= warm:
             times.append(full)
     t = statistics.median(times)
