@@ -423,7 +423,8 @@ def run_ours(args, cfg):
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:
-            full, desc = oracle_sample(cfg, 16, 400000)
+            # ~4 s of fp64 BLAS at K = 6144; fewer rows for longer transfer rows (host memory)
+            full, desc = oracle_sample(cfg, 16, max(2000, 400000 * 6144 // (cfg.faces * cfg.k_face)))
             line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                                     "sample": desc}
         print(json.dumps(line), flush=True)

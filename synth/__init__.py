@@ -382,6 +382,8 @@ CONFIGS = {
     "c3": Config("c3", 6, 6, 10000, 6, 1, SEED_BASE + 3, "6x64x64 cube map, 10k vertices, per-frame global shift + relight"),
     "c4": Config("c4", 7, 6, 100000, 7, 1, SEED_BASE + 4, "6x128x128 cube map, 100k vertices, per-vertex shifts"),
     "c5": Config("c5", 8, 6, 1000000, 5, 64, SEED_BASE + 5, "6x256x256 cube map, 1M vertices, 64 frames"),
+    "c5x": Config("c5x", 8, 6, 1000000, 6, 64, SEED_BASE + 5,
+                  "c5 stress variant (SURVEY §8(d)): transfer 6 x 4096 coefficients per vertex (98.3 GB)"),
     "c5s": Config("c5s", 8, 6, 1000000, 8, 64, SEED_BASE + 5,
                   "c5 with sparse top-K transfer (K_s = 256 full-resolution coefficients per vertex, row f2)",
                   {"k_sparse": 256, "dense_levels": 2}),
