@@ -97,33 +97,24 @@ __global__ void rot_topdown_kernel(const float* __restrict__ in, long long maps,
 }
 
 // ------------------------------------------------------------------------------- (2) chain rule
-struct Jac {
-  float Th, Ph;          // rotated angles
-  float Tt, Tp, Pt, Pp;  // dTheta/dtheta, dTheta/dphi, dPhi/dtheta, dPhi/dphi
+// (Theta, Phi) of R_x(alpha) p(theta, phi): eq:theta / eq:phi, Phi in [0, 2 pi)
+struct Ang {
+  float Th, Ph;
 };
 
-__device__ __forceinline__ Jac rotated(float th, float ph, float ca, float sa) {
+__device__ __forceinline__ Ang rotated(float th, float ph, float ca, float sa) {
   float st, ct, sp, cp;
   sincosf(th, &st, &ct);
   sincosf(ph, &sp, &cp);
   const float a = st * sp;                   // x' = x
   const float u = ca * ct - sa * st * cp;    // y' = cos Theta
   const float b = sa * ct + ca * st * cp;    // z'
-  Jac J;
-  J.Th = acosf(fminf(1.f, fmaxf(-1.f, u)));
+  Ang r;
+  r.Th = acosf(fminf(1.f, fmaxf(-1.f, u)));
   float P = atan2f(a, b);
   if (P < 0.f) P += 6.283185307179586f;
-  J.Ph = P;
-  const float s2 = fmaxf(a * a + b * b, 1e-12f);   // sin^2 Theta
-  const float is = rsqrtf(s2);
-  const float u_t = -ca * st - sa * ct * cp, u_p = sa * st * sp;
-  J.Tt = -u_t * is;
-  J.Tp = -u_p * is;
-  const float a_t = ct * sp, a_p = st * cp;
-  const float b_t = -sa * st + ca * ct * cp, b_p = -ca * st * sp;
-  J.Pt = (b * a_t - a * b_t) / s2;
-  J.Pp = (b * a_p - a * b_p) / s2;
-  return J;
+  r.Ph = P;
+  return r;
 }
 
 // bilinear sample of a field plane (rows 0..R-1) extended by the reflected rows lo (row -1) and
@@ -177,12 +168,12 @@ __global__ void rot_chainrule_kernel(const float* __restrict__ F, const float* _
     const float* Xf = F + b * 2 * NN;
     const float* Yf = Xf + NN;
     const float* Eb = E + b * 4 * N;
-    const Jac A0 = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
+    const Ang A0 = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
       const float di = t ? 1.f : 0.f, dj = t ? 0.f : 1.f;
-      const Jac A1 = rotated(((float)i + 0.5f + di) * kT, ((float)j + 0.5f + dj) * kP, ca, sa);
-      const Jac M = rotated(((float)i + 0.5f + 0.5f * di) * kT, ((float)j + 0.5f + 0.5f * dj) * kP, ca, sa);
+      const Ang A1 = rotated(((float)i + 0.5f + di) * kT, ((float)j + 0.5f + dj) * kP, ca, sa);
+      const Ang M = rotated(((float)i + 0.5f + 0.5f * di) * kT, ((float)j + 0.5f + 0.5f * dj) * kP, ca, sa);
       const float y = M.Th * iT - 0.5f, x = M.Ph * iP - 0.5f;
       const float xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5f);           // X_f lives at (i, j + 1/2)
       const float yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5f, x);  // Y_f at (i + 1/2, j)
@@ -294,7 +285,7 @@ __global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ i
   float acc = 0.f;
   for (long long p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = (int)(p >> n), j = (int)(p & (N - 1));
-    const Jac J = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
+    const Ang J = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
     const float y = J.Th * (float)M / 3.14159265358979f - 0.5f;   // in [-1/2, M - 1/2]
     const float x = J.Ph * (float)M / 6.283185307179586f - 0.5f;
     const float fy = floorf(y), fx = floorf(x);
