@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunks", type=int, default=4)
     p.add_argument("--e2e-chunks", type=int, default=4)
+    p.add_argument("--no-graph", action="store_true", help="c2: direct launches instead of a CUDA graph")
     p.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                    help="N>1: fused relight + gather into rank 0's buffer over NVLink (p2p) or NCCL gather")
     p.add_argument("--start-level", type=int, default=None,
@@ -549,10 +550,41 @@ def run_aux(args, cfg):
         evs.append((a_, b_))
         return out
 
+    graph = None
+    if cfg.name == "c2" and not args.no_graph:
+        # c2 is launch-latency bound: capture one step (shift + relight, fixed shift) in a CUDA graph
+        # after the warm-up and replay it; the L2 flush stays outside the graph and outside the timing
+        def step_graph(i):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            dom.append((e0, e1))
+            launches["n"] += graph_launches
+            return R
+
     step_ev = []
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    if cfg.name == "c2" and not args.no_graph:
+        s_cap = torch.cuda.Stream(dev)
+        s_cap.wait_stream(stream)
+        n0 = launches["n"]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s_cap):
+            sh0 = np.broadcast_to(frames[0][None, None, :], (1, F, 2))
+            hs.haar_shift_coeffs(light, sh0, 2, out=shifted, workspace=ws)
+            launches["n"] += hs.last_launch_count()
+            hs.relight_vertices(T, shifted, F, kf, out=R)
+            launches["n"] += hs.last_launch_count()
+        graph_launches = launches["n"] - n0
+        kernel_name = "shift + relight (one CUDA graph replay: 4 kernels)"
+        stream.wait_stream(s_cap)
+        for i in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+        step = step_graph
     launches["n"] = 0
     dom.clear()
     if world > 1:
