@@ -35,8 +35,9 @@
 //   coarse_finish_kernel  one CTA per face: the coarse bottom-up c -> 0 from the shifted fields.
 // Levels >= m (dyadic shifts) are exact permutations (permute_kernel).
 //
-// Field precision FT: fp32 for log2n <= 8; fp64 above (DESIGN.md §4.1 error model: fine-level
-// fp32 rounding is amplified ~2^(n-l) on the coarse outputs of large faces).
+// Field precision FT: fp32 for log2n <= 7; fp64 above (DESIGN.md §4.1 error model: fine-level
+// fp32 rounding is amplified ~2^(n-l) on the coarse outputs of large faces; at N = 256 the
+// relight band of the c5 light reached 1.3e-5 per frame in fp32, 3e-8 in fp64).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -762,7 +763,7 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
 
 }  // namespace
 
-bool shift2d_uses_fp64(int log2n) { return log2n >= 9; }
+bool shift2d_uses_fp64(int log2n) { return log2n >= 8; }
 
 hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, cudaStream_t st) {
   if (max_tiles > 0) {
