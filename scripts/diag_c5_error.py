@@ -7,7 +7,7 @@ sys.path.insert(0, os.getcwd())
 import synth
 import paper_1705_07272_b200 as hs
 from oracle import relight as orelight, shift as oshift
-cfg = synth.config("c5")
+cfg = synth.config(sys.argv[1] if len(sys.argv) > 1 else "c5")
 V, F, n, B, kf = 20000, cfg.faces, cfg.log2n, cfg.frames, cfg.k_face
 T = torch.empty((V, F * kf), dtype=torch.float32, device="cuda")
 hs.hs_fill_transfer(T, 0, F, kf, cfg.seed, synth.STREAM_T)
