@@ -32,7 +32,8 @@
 //     warp 2  TMEM allocator
 //     warps 4-7  converters: evaluate the tripling terms of their row's chunk from smem, split
 //                fp32 -> fp16 hi/lo, tcgen05.st into the A stage -- M never touches HBM
-//     warps 8-11 epilogue (both accumulators, per-frame scale), as in relight_tc.cu
+//     warps 8-11 epilogue: drains each 16-k-block accumulation group into fp32 registers, then
+//                the per-frame scale, as in relight_tc.cu
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -188,6 +189,7 @@ constexpr int BM = 128, BK = 64, BN = 64;
 constexpr int DSTAGES = 3;                      // rho + V tiles
 constexpr int LSTAGES = 2;                      // light tiles
 constexpr int ASTAGES = 4;                      // TMEM A stages
+constexpr int KG = 16;                          // k-blocks per accumulation group (relight_tc.cu)
 constexpr int T_TILE = BM * BK * 4;             // 32 KB per operand tile
 constexpr int D_STAGE = 2 * T_TILE;             // rho | V
 constexpr int L_STAGE = kTcLTileBytes;          // 16 KB
@@ -298,15 +300,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int lstage = 0, astage = 0;
       uint32_t lphase = 0, aphase = 0;
-      int it = 0;
+      int gi = 0;   // accumulation group (KG k-blocks) counter: buffer gi & 1
       const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
-      for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t accph = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], accph ^ 1);
-        fence_after();
-        const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
+      for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb) {
+          const int acc = gi & 1;
+          const bool first = (kb % KG) == 0;
+          if (first) {
+            mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
+            fence_after();
+          }
+          const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
           mbar_wait(&lfull[lstage], lphase);
           mbar_wait(&afull[astage], aphase);
           fence_after();
@@ -315,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bd = sw128_desc(lbase + kk * 32);
             const uint32_t ahi = tmem + astage * 64 + kk * 8;
-            tc_mma_ts(dhh, ahi, bd, id128, (kb | kk) != 0);      // [acc_hh | acc_x] += M_hi x [L_hi | L_lo]
-            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);          // acc_x += M_lo x L_hi
+            tc_mma_ts(dhh, ahi, bd, id128, (!first || kk) ? 1u : 0u);   // [acc_hh | acc_x] += M_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);                  // acc_x += M_lo x L_hi
           }
           tc_commit(&lempty[lstage]);
           tc_commit(&aempty[astage]);
@@ -328,8 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             astage = 0;
             aphase ^= 1;
           }
+          if ((kb % KG) == KG - 1 || kb == nkb - 1) {
+            tc_commit(&tfull[acc]);   // group complete: the epilogue drains it into registers
+            ++gi;
+          }
         }
-        tc_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -386,35 +393,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = threadIdx.x - 256;
     const int q = warp & 3;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    int it = 0;
-    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
+    int gi = 0;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
       const int tile = (int)(w / nfb), fb = (int)(w % nfb);
-      const int acc = it & 1;
-      const uint32_t accph = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], accph);
-      fence_after();
       const long long grow = (long long)tile * BM + row;
-      float* out = R + grow * B + fb * BN;
+      float sum[BN];
 #pragma unroll
-      for (int c = 0; c < BN / 16; ++c) {
-        float hh[16], xx[16];
-        tmem_ld16(lane_base + ACC_COL0 + acc * 128 + c * 16, hh);
-        tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
-        tmem_wait_ld();
-        if (grow < V) {
+      for (int j = 0; j < BN; ++j) sum[j] = 0.f;
+      for (int g0 = 0; g0 < nkb; g0 += KG, ++gi) {
+        const int acc = gi & 1;
+        mbar_wait(&tfull[acc], (gi >> 1) & 1);
+        fence_after();
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            float4 o;
-            o.x = fmaf(xx[j + 0], 1.f / 2048.f, hh[j + 0]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 0);
-            o.y = fmaf(xx[j + 1], 1.f / 2048.f, hh[j + 1]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 1);
-            o.z = fmaf(xx[j + 2], 1.f / 2048.f, hh[j + 2]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 2);
-            o.w = fmaf(xx[j + 3], 1.f / 2048.f, hh[j + 3]) * __ldg(inv_scale_g + fb * BN + c * 16 + j + 3);
-            *reinterpret_cast<float4*>(out + c * 16 + j) = o;
-          }
+        for (int c = 0; c < BN / 16; ++c) {
+          float hh[16], xx[16];
+          tmem_ld16(lane_base + ACC_COL0 + acc * 128 + c * 16, hh);
+          tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += fmaf(xx[j], 1.f / 2048.f, hh[j]);
+        }
+        fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
+      if (grow < V) {
+        float* out = R + grow * B + fb * BN;
+#pragma unroll
+        for (int j = 0; j < BN; j += 4) {
+          float4 o;
+          o.x = sum[j + 0] * __ldg(inv_scale_g + fb * BN + j + 0);
+          o.y = sum[j + 1] * __ldg(inv_scale_g + fb * BN + j + 1);
+          o.z = sum[j + 2] * __ldg(inv_scale_g + fb * BN + j + 2);
+          o.w = sum[j + 3] * __ldg(inv_scale_g + fb * BN + j + 3);
+          *reinterpret_cast<float4*>(out + j) = o;
         }
       }
-      fence_before();
-      mbar_arrive(&tempty[acc]);
     }
   }
   fence_before();
