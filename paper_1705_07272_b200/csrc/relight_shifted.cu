@@ -29,45 +29,47 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 
 // ------------------------------------------------------------------------------- prep
 // fields[f][t][parity][r][c/2] = F_n[r][c] for t in {X, Y, Z}; one CTA per face, top-down over the
-// whole (periodic) grid, level by level, ping-ponging through the scratch area.
+// whole (periodic) grid, level by level, ping-ponging through the scratch area.  The recursion
+// runs in fp64 and each field value is rounded to fp32 once: fp32 recursion accumulates an
+// absolute error ~eps |A| (pixel-value scale, ~1e4 for HDR suns) into every difference.
 __global__ void __launch_bounds__(kThreads) fields_kernel(const float* __restrict__ light, int n,
-                                                          float* __restrict__ fields, float* __restrict__ scratch) {
+                                                          float* __restrict__ fields, double* __restrict__ scratch) {
   const int f = blockIdx.x;
   const int N = 1 << n;
   const long long NN = (long long)N * N;
   const float* in = light + (long long)f * NN;
-  float* buf[2] = {scratch + (long long)f * 6 * NN, scratch + (long long)f * 6 * NN + 3 * NN};
+  double* buf[2] = {scratch + (long long)f * 6 * NN, scratch + (long long)f * 6 * NN + 3 * NN};
   // level 0 fields are 0; level l+1 from level l
   for (int l = 0; l < n; ++l) {
     const int g = 1 << l, G = 2 * g;
-    const float asc = pow2f(l);
-    const float* cur = buf[l & 1];
+    const double asc = (double)pow2f(l);
+    const double* cur = buf[l & 1];
     const bool last = (l + 1 == n);
-    float* nxt = buf[(l + 1) & 1];
+    double* nxt = buf[(l + 1) & 1];
     for (int idx = threadIdx.x; idx < g * g; idx += blockDim.x) {
       const int i = idx >> l, j = idx & (g - 1);
-      float d[2][2][2][2];
+      double d[2][2][2][2];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int ii = (i + u) & (g - 1), jj = (j + v) & (g - 1);
           const long long o = (long long)ii * g + jj;
-          const float H = __ldg(in + (long long)g * g * 1 + o) * asc;
-          const float V = __ldg(in + (long long)g * g * 2 + o) * asc;
-          const float D = __ldg(in + (long long)g * g * 3 + o) * asc;
+          const double H = (double)__ldg(in + (long long)g * g * 1 + o) * asc;
+          const double V = (double)__ldg(in + (long long)g * g * 2 + o) * asc;
+          const double D = (double)__ldg(in + (long long)g * g * 3 + o) * asc;
           d[u][v][0][0] = H + V + D;
           d[u][v][0][1] = -H + V - D;
           d[u][v][1][0] = H - V - D;
           d[u][v][1][1] = -H - V + D;
         }
-      float Xl = 0.f, Yl = 0.f, Zl = 0.f;
+      double Xl = 0.0, Yl = 0.0, Zl = 0.0;
       if (l > 0) {
         Xl = __ldcg(cur + idx);
         Yl = __ldcg(cur + g * g + idx);
         Zl = __ldcg(cur + 2 * g * g + idx);
       }
-      float cx[2][2], cy[2][2], cz[2][2];
+      double cx[2][2], cy[2][2], cz[2][2];
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
         cx[a][0] = d[0][0][a][0] - d[0][0][a][1];
@@ -96,9 +98,9 @@ __global__ void __launch_bounds__(kThreads) fields_kernel(const float* __restric
             // final layout: [f][t][parity][r][c/2]
             float* base = fields + (long long)f * 3 * NN;
             const long long o = (long long)(c & 1) * (NN / 2) + (long long)r * (N / 2) + (c >> 1);
-            base[o] = cx[a][b];
-            base[NN + o] = cy[a][b];
-            base[2 * NN + o] = cz[a][b];
+            base[o] = (float)cx[a][b];
+            base[NN + o] = (float)cy[a][b];
+            base[2 * NN + o] = (float)cz[a][b];
           }
         }
     }
@@ -457,7 +459,7 @@ bool relight_shifted_fused_supported(int log2n) { return log2n >= 5 && log2n <= 
 
 size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n) {
   const size_t NN = (size_t)1 << (2 * log2n);
-  return (size_t)faces * 3 * NN * 4 /*fields*/ + (size_t)faces * 6 * NN * 4 /*scratch*/ +
+  return (size_t)faces * 3 * NN * 4 /*fields*/ + (size_t)faces * 6 * NN * 8 /*fp64 scratch*/ +
          (size_t)V * 3 * faces * 4 /*partials*/ + (size_t)V * 16 /*vertex params*/ + 512;
 }
 
@@ -465,8 +467,8 @@ hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, c
                                        const float* shifts, float* R, void* ws, cudaStream_t st) {
   const size_t NN = (size_t)1 << (2 * log2n);
   float* fields = reinterpret_cast<float*>(ws);
-  float* scratch = fields + (size_t)faces * 3 * NN;
-  float* partial = scratch + (size_t)faces * 6 * NN;
+  double* scratch = reinterpret_cast<double*>(fields + (size_t)faces * 3 * NN);
+  float* partial = reinterpret_cast<float*>(scratch + (size_t)faces * 6 * NN);
   int4* vp = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(partial + (size_t)V * 3 * faces) + 255) & ~uintptr_t(255));
   fields_kernel<<<faces, kThreads, 0, st>>>(light, log2n, fields, scratch);
   HS_CHECK_LAUNCH("fields_kernel");

@@ -39,6 +39,7 @@ def test_c5_full_size_sampled_rows():
     band = oshift.shift_coeffs(light_np, shifts, 2, band_levels=cfg.band_levels)
     ref = np.concatenate([orelight.relight(synth.transfer_rows(cfg.seed, int(v), 1, F, kf), band, F, kf)
                           for v in rows])
+    print(f"c5 full size: rel-L2 {_rel(got, ref):.3e}")
     assert _rel(got, ref) <= TOL
 
 
@@ -59,4 +60,5 @@ def test_c4_full_size_sampled_vertices():
     del T
     ref = np.array([orelight.relight_shifted(synth.transfer_rows(cfg.seed, int(v), 1, F, 4 ** n), L,
                                              sv[v:v + 1].astype(np.float64))[0] for v in rows])
+    print(f"c4 full size: rel-L2 {_rel(got, ref):.3e}")
     assert _rel(got, ref) <= TOL
