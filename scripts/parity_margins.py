@@ -1,0 +1,73 @@
+"""Parity margins (not a test): relative L2 error against the fp64 oracle of every benchmarked
+configuration, on the bench's inputs and launch configurations (sampled vertices where the oracle
+cannot afford all of them).  Output: one line per config; the gate is 1e-5."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_1705_07272_b200 as hs  # noqa: E402
+from oracle import relight as orelight  # noqa: E402
+from oracle import shift as oshift  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def t(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+out = {}
+rng = np.random.default_rng(2024)
+# c2: one 32x32 map, shift (3.25, 7.5), 1k vertices
+cfg = synth.config("c2")
+L = synth.light_pyramids(cfg.seed, 1, 1, cfg.log2n)
+sh = np.array([[[3.25, 7.5]]])
+T = synth.transfer_rows(cfg.seed, 0, cfg.vertices, 1, cfg.k_face)
+band = hs.haar_shift_coeffs(t(L), sh, 2)
+R = hs.relight_vertices(t(T), band, 1, cfg.k_face).cpu().numpy()
+out["c2 radiance"] = rel(R, orelight.relight(T, oshift.shift_coeffs(L, sh, 2), 1, cfg.k_face))
+# c3: 10k vertices, frames 0, 37, 200 (1-degree azimuth steps)
+cfg = synth.config("c3")
+L = synth.light_pyramids(cfg.seed, 1, cfg.faces, cfg.log2n)
+T = synth.transfer_rows(cfg.seed, 0, cfg.vertices, cfg.faces, cfg.k_face)
+worst = 0.0
+for fr in (1, 37, 200):
+    sh = np.broadcast_to(synth.c3_shifts(cfg.log2n, 360)[fr][None, None, :], (1, cfg.faces, 2))
+    band = hs.haar_shift_coeffs(t(L), sh, 2)
+    R = hs.relight_vertices(t(T), band, cfg.faces, cfg.k_face).cpu().numpy()
+    worst = max(worst, rel(R, orelight.relight(T, oshift.shift_coeffs(L, sh, 2), cfg.faces, cfg.k_face)))
+out["c3 radiance (3 frames, worst)"] = worst
+# c5-shaped light (64 frames of 6 x 256^2) shared by c5x / c5s / c5t
+cfg5 = synth.config("c5")
+B, F, n = cfg5.frames, cfg5.faces, cfg5.log2n
+light_np = synth.light_pyramids(cfg5.seed, B, F, n)
+sh5 = np.broadcast_to(synth.c5_shifts(cfg5.seed, B, n)[:, None, :], (B, F, 2)).copy()
+full = hs.haar_shift_coeffs(t(light_np), sh5, 2)
+ref_full = oshift.shift_coeffs(light_np, sh5, 2)
+out["c5 shifted pyramids (64 frames, full)"] = rel(full.cpu().numpy(), ref_full)
+out["c5 shifted band (levels < 5)"] = rel(full.cpu().numpy()[:, :, :1024], ref_full[:, :, :1024])
+for name, kf in (("c5", 1024), ("c5x", 4096)):
+    rows = rng.integers(0, 1_000_000, 96)
+    T = np.concatenate([synth.transfer_rows(cfg5.seed, int(v), 1, F, kf) for v in rows])
+    R = hs.relight_vertices(t(T), full, F, kf).cpu().numpy()
+    out[f"{name} radiance (96 sampled vertices)"] = rel(R, orelight.relight(T, ref_full, F, kf))
+# c5s: sparse K_s = 256 over the full pyramids
+idx, val = synth.sparse_transfer_rows(cfg5.seed, 0, 3000, F, n, 256, 2)
+R = hs.relight_vertices_sparse(torch.from_numpy(idx).cuda(), t(val), full).cpu().numpy()
+out["c5s radiance (3000 vertices)"] = rel(R, orelight.relight_sparse(idx, val, ref_full.reshape(B, -1)))
+# c5t: triple product on the band
+rho = synth.shading_rows(cfg5.seed, 0, 2000, F, 1024, synth.STREAM_BRDF)
+vis = synth.shading_rows(cfg5.seed, 0, 2000, F, 1024, synth.STREAM_VIS)
+rq = hs.haar_pack_qtree(t(rho).view(2000, F, 1024), 5)
+vq = hs.haar_pack_qtree(t(vis).view(2000, F, 1024), 5)
+R = hs.relight_vertices_triple(rq, vq, full, F, 1024).cpu().numpy()
+out["c5t radiance (2000 vertices)"] = rel(R, orelight.relight_triple(rho, vis, ref_full[:, :, :1024], F, 1024))
+torch.cuda.synchronize()
+for k, v in out.items():
+    print(f"{k:42s} {v:.3e}  ({'ok' if v <= 1e-5 else 'OVER'}; margin x{1e-5 / v:.1f})")
