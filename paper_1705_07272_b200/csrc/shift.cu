@@ -116,7 +116,6 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
                        const float* shifts_dev_per_vertex, FaceParam* dev_fp_buf, int band,
                        void* ws, size_t ws_bytes, cudaStream_t st) {
   const int n = log2n;
-  const long long K = (ndim == 2) ? (1ll << (2 * n)) : (1ll << n);
   const long long Kb = (ndim == 2) ? (1ll << (2 * band)) : (1ll << band);
   float* wsf = nullptr;
   const long long wsface = (ndim == 2) ? ws_face_floats_2d(n) : 0;

@@ -234,7 +234,6 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   using S = TSmem<FT, K, TC>;
   constexpr int CB = G::CB, HC = G::HC, CHR = G::CHR, SN1 = G::SN1;
   constexpr int PLANE_C = CHR * HC;  // one parity plane of one field's children
-  const int n = args.log2n;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in =
       args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
