@@ -241,6 +241,10 @@ def run_ours(args, cfg):
         raise SystemExit("--start-level is a single-GPU option")
     R = torch.empty((rows, B), dtype=torch.float32, device=dev)
     R_full = torch.empty((V, B), dtype=torch.float32, device=dev) if (rank == 0 and world > 1) else None
+    fs0, fsn = hsdist.shard_rows(B, world, rank)          # this rank's frames of the sharded shift
+    band_local = torch.empty((fsn, F, kf), dtype=torch.float32, device=dev) if world > 1 else None
+    if world > 1:
+        ws = torch.empty(max(1, hs.haar_shift_workspace_bytes(2, n, F, max(fsn, 1))), dtype=torch.uint8, device=dev)
     gather_mode = args.gather if world > 1 else "none"
     R_view = None
     if gather_mode == "p2p":
@@ -275,6 +279,24 @@ def run_ours(args, cfg):
 
     def step():
         """One pass of the hot path; returns this rank's result tensor (R, or R_full on rank 0)."""
+        if world > 1:
+            # shift sharded by frame, band all-gathered over NVLink
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hs.haar_shift_coeffs(light[fs0:fs0 + fsn], shifts[fs0:fs0 + fsn], 2, cfg.band_levels, out=band_local,
+                                 workspace=ws)
+            e1.record(stream)
+            shift_events.append((e0, e1))
+            launches["n"] += hs.last_launch_count()
+            hsdist.allgather_band(band_local, shifted)
+            if gather_mode == "p2p":
+                hsdist.relight_into_peer(T, shifted, V, relight_fn, R_view)
+                stream.synchronize()
+                dist.barrier()              # every rank's rows are in rank 0's buffer
+                return R_full
+            _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
+            return full
         if rank == 0:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -287,15 +309,6 @@ def run_ours(args, cfg):
             e1.record(stream)
             shift_events.append((e0, e1))
             launches["n"] += hs.last_launch_count()
-        if world > 1:
-            hsdist.broadcast_band(shifted)
-            if gather_mode == "p2p":
-                hsdist.relight_into_peer(T, shifted, V, relight_fn, R_view)
-                stream.synchronize()
-                dist.barrier()              # every rank's rows are in rank 0's buffer
-                return R_full
-            _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
-            return full
         relight_fn(T, shifted_band if args.start_level is not None else shifted, R)
         return R
 
@@ -375,8 +388,7 @@ def run_ours(args, cfg):
         Rh = torch.empty((out_rows, B), dtype=torch.float32).pin_memory()
 
         def e2e_step():
-            if rank == 0:
-                light.copy_(light_h, non_blocking=True)
+            light[fs0:fs0 + fsn].copy_(light_h[fs0:fs0 + fsn], non_blocking=True)   # this rank's frames
             res = step()
             if res is not None and rank == 0:
                 Rh.copy_(res, non_blocking=True)
@@ -397,10 +409,11 @@ def run_ours(args, cfg):
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": V / (float(e_ms.item()) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(light_np.nbytes) if rank == 0 else 0,
+               "h2d_bytes_per_step": int(light_np[fs0:fs0 + fsn].nbytes),
                "d2h_bytes_per_step": int(out_rows * B * 4),
-               "note": "per step: pinned H2D of the 64 light pyramids + shift + relight (+ gather) + D2H of "
-                       "the full radiance on rank 0; T is scene data resident in HBM"}
+               "note": "per step: pinned H2D of each rank's own light frames (rank 0's bytes shown) + sharded "
+                       "shift + band all-gather + relight + gather + D2H of the full radiance on rank 0; T is "
+                       "scene data resident in HBM"}
 
     if rank == 0:
         line = {
@@ -416,7 +429,7 @@ def run_ours(args, cfg):
                          "avg_launch_ms": avg_ms, "share_of_step": sum(rel_ms) / args.steps / ms},
             "shift_ms": (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events)) if shift_events else None,
             "shift_start_level": args.start_level,
-            "shift_frac_hbm": ((2 * B * F * N * N * 4 if full_out else B * F * (N * N + kf) * 4) /
+            "shift_frac_hbm": ((2 * B * F * N * N * 4 if full_out else fsn * F * (N * N + kf) * 4) /
                                (sum(a.elapsed_time(b) for a, b in shift_events) / len(shift_events) * 1e-3) / 1e9 / peak)
             if shift_events else None,
             "gpu_launches": gpu_launches,

@@ -5,8 +5,9 @@ One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
 * vertex rows are contiguous blocks [start_r, start_r + count_r) per rank (``shard_rows``); the
   transfer rows T are generated in place on their rank from the counter hash keyed by the GLOBAL
   row id, so every shard is bitwise the 1-GPU matrix's slice and never moves;
-* the shifted lighting band is computed once (rank 0, ``haar_shift_coeffs``) and broadcast
-  (``dist.broadcast`` over NVLink) -- the one exchange step into the relight;
+* the shifted lighting band is computed sharded by frame (each rank shifts its ``frame_shard`` of the
+  batch) and all-gathered (``allgather_band``, NCCL over NVLink) -- the one exchange step into the
+  relight; ``broadcast_band`` (rank 0 shifts everything) is kept for single-frame batches;
 * radiance reaches rank 0 in one of two ways:
   - fused (``open_peer_view`` + ``relight_into_peer``, the default of bench.py): rank 0's radiance
     buffer is opened in every rank through CUDA IPC and each rank's relight kernel stores its
@@ -59,6 +60,37 @@ def broadcast_band(band: torch.Tensor, src: int = 0, group=None) -> torch.Tensor
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.broadcast(band, src=src, group=group)
     return band
+
+
+def frame_shard(batch: int, group=None) -> Tuple[int, int]:
+    """This rank's contiguous block of light frames for the sharded shift ([start, start+count))."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    return shard_rows(batch, world, rank)
+
+
+def allgather_band(band_local: torch.Tensor, band_full: torch.Tensor, group=None) -> torch.Tensor:
+    """The shift sharded by frame: every rank shifted its ``frame_shard`` frames into ``band_local``
+    ([count][faces][stride]); gather all of them into ``band_full`` ([batch][faces][stride]) on every
+    rank.  Equal shards go through one all_gather_into_tensor (NCCL over NVLink); uneven ones are
+    padded to the largest shard."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    B = band_full.shape[0]
+    if world == 1:
+        band_full.copy_(band_local)
+        return band_full
+    ms = max_shard(B, world)
+    if B % world == 0:
+        dist.all_gather_into_tensor(band_full, band_local.contiguous(), group=group)
+        return band_full
+    pad = torch.zeros((ms,) + tuple(band_local.shape[1:]), dtype=band_local.dtype, device=band_local.device)
+    pad[: band_local.shape[0]].copy_(band_local)
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    for r in range(world):
+        s, c = shard_rows(B, world, r)
+        band_full[s:s + c].copy_(parts[r][:c])
+    return band_full
 
 
 def relight_and_gather(transfer_local: torch.Tensor, band: torch.Tensor, total_rows: int,

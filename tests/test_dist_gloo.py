@@ -95,3 +95,41 @@ def test_chunk_bounds():
     assert hsdist.chunk_bounds(0, 4) == []
     with pytest.raises(ValueError):
         hsdist.shard_rows(10, 2, 2)
+
+
+def _band_worker(rank, world, port, B, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(3)
+        full = torch.randn(B, 6, 16, generator=g)
+        s, c = hsdist.frame_shard(B)
+        assert (s, c) == hsdist.shard_rows(B, world, rank)
+        got = torch.full_like(full, float("nan"))
+        hsdist.allgather_band(full[s:s + c].clone(), got)
+        q.put(("ok", rank, bool(torch.equal(got, full))))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), rank))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,B", [(2, 64), (3, 64), (2, 5)])
+def test_sharded_shift_band_allgather(world, B):
+    """every rank shifts its frames; the all-gathered band equals the unsharded one on every rank
+    (equal shards: one all_gather_into_tensor; uneven: padded all_gather)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), msgs
+    assert len([m for m in msgs if m[0] == "ok" and m[2]]) == world, msgs
