@@ -115,7 +115,7 @@ struct ShiftArgs {
   const FaceParam* dev_fp;    // device FaceParams (per-vertex path) or nullptr -> use fp[]
   long long in_batch_stride;  // elements; 0 broadcasts one pyramid set to every batch entry
   long long in_face_stride;   // elements between the faces of one batch entry (>= K)
-  long long ws_face_stride;   // floats per face in ws
+  long long ws_face_stride;   // BYTES per face in ws (ws_face_floats_2d doubles)
   int log2n, faces, band, out_face_stride, num_faces;
   FaceParam fp[kMaxFacesPerLaunch];
 };
@@ -126,8 +126,9 @@ constexpr int kTileTC = 8;    // tile side at level c (cells)
 
 inline int coarse_level(int m) { return m > kTileKF ? m - kTileKF : 0; }
 bool shift2d_uses_fp64(int log2n);        // field precision of the 2D tile kernel
-inline long long ws_face_floats_2d(int n) {  // elements of the field type per face
-  // [shifted level-c fields 3*4^c][unshifted level-c fields 3*4^c][scratch 3*4^(c-1)]
+inline long long ws_face_floats_2d(int n) {  // 8-byte elements per face
+  // [shifted level-c fields 3*4^c (tile field type)][unshifted level-c fields 3*4^c (fp64)]
+  // [scratch 3*4^(c-1)]
   int c = coarse_level(n);
   if (c == 0) return 0;
   return 6ll * (1ll << (2 * c)) + 3ll * (1ll << (2 * (c - 1)));

@@ -105,8 +105,7 @@ __global__ void face_params_kernel(const float* __restrict__ shifts, long long n
 
 size_t shift_workspace_bytes_impl(int ndim, int log2n, long long num_faces) {
   if (ndim != 2) return 0;
-  const size_t esz = shift2d_uses_fp64(log2n) ? 8 : 4;
-  return (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * esz;
+  return (size_t)num_faces * (size_t)ws_face_floats_2d(log2n) * 8;
 }
 
 // in:  [num_faces / faces batches][faces][K]; out [num_faces][Kb]
@@ -118,7 +117,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
   const int n = log2n;
   const long long Kb = (ndim == 2) ? (1ll << (2 * band)) : (1ll << band);
   float* wsf = nullptr;
-  const long long wsface = (ndim == 2) ? ws_face_floats_2d(n) : 0;
+  const long long wsface = (ndim == 2) ? ws_face_floats_2d(n) * 8 : 0;   // bytes per face
   if (ndim == 2) wsf = reinterpret_cast<float*>(ws);
   const long long batches = num_faces / faces;
   const long long chunk_b = std::max<long long>(1, kMaxFacesPerLaunch / faces);
@@ -129,9 +128,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     const long long g0 = b0 * faces;
     a.in = in + b0 * in_batch_stride;
     a.out = out + g0 * Kb;
-    a.ws = wsf ? reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) +
-                                         g0 * wsface * (shift2d_uses_fp64(n) ? 8 : 4))
-               : nullptr;
+    a.ws = wsf ? reinterpret_cast<float*>(reinterpret_cast<char*>(wsf) + g0 * wsface) : nullptr;
     a.dev_fp = nullptr;
     a.in_batch_stride = in_batch_stride;
     a.in_face_stride = in_face_stride;

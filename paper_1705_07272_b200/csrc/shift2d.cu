@@ -274,18 +274,6 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
   //      group B is still in flight.  Per level d = m - l the window side is a compile-time
   //      constant, so the element decode uses constant divisors.
   load_windows<G, 3, K>(in, sDet, sR, sDoff, m);             // group A: d = 3 .. K (levels c .. m-3)
-  if (c > 0) {                                                 // group A: unshifted level-c fields
-    const int gc = 1 << c, cm = gc - 1;
-    const int pw = sR[0][1][c], ys = sR[0][0][c], xs = sR[1][0][c];
-    const FT* src = reinterpret_cast<const FT*>(args.ws) + (long long)g * args.ws_face_stride + 3ll * gc * gc;
-    FT* dst = sCh + ((((K - 2) & 1) == 0) ? 3 * G::ANC_MAX * G::ANC_MAX : 0);
-    for (int e = tid; e < 3 * pw * pw; e += kThreads) {
-      const int t = e / (pw * pw), rem = e - t * pw * pw;
-      const int a = rem / pw, bb = rem - a * pw;
-      cp_async_ft<FT>(dst + t * G::ANC_MAX * G::ANC_MAX + a * pw + bb,
-                      src + (long long)t * gc * gc + (long long)((ys + a) & cm) * gc + ((xs + bb) & cm));
-    }
-  }
   cp_async_commit();
   if (m - 1 >= 2)
     load_window_vec<G>(in, sDet, sR, sDoff, m);               // group B: d = 1 (16-byte chunks)
@@ -293,6 +281,19 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
     load_windows<G, 1, 1>(in, sDet, sR, sDoff, m);
   load_windows<G, 2, 2>(in, sDet, sR, sDoff, m);             // group B: d = 2
   cp_async_commit();
+  if (c > 0) {  // unshifted level-c fields (fp64, coarse_fields_kernel) -> FT, while the copies fly
+    const int gc = 1 << c, cm = gc - 1;
+    const int pw = sR[0][1][c], ys = sR[0][0][c], xs = sR[1][0][c];
+    const double* src = reinterpret_cast<const double*>(reinterpret_cast<const char*>(args.ws) +
+                                                        (long long)g * args.ws_face_stride + 3ll * gc * gc * 8);
+    FT* dst = sCh + ((((K - 2) & 1) == 0) ? 3 * G::ANC_MAX * G::ANC_MAX : 0);
+    for (int e = tid; e < 3 * pw * pw; e += kThreads) {
+      const int t = e / (pw * pw), rem = e - t * pw * pw;
+      const int a = rem / pw, bb = rem - a * pw;
+      dst[t * G::ANC_MAX * G::ANC_MAX + a * pw + bb] =
+          FT(__ldcg(src + (long long)t * gc * gc + (long long)((ys + a) & cm) * gc + ((xs + bb) & cm)));
+    }
+  }
   cp_async_wait_group1();                                    // A complete, B may be in flight
   __syncthreads();
 
@@ -546,7 +547,7 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
 
   // ---- publish the owned shifted level-c fields (coarse_finish_kernel runs the bottom-up c -> 0)
   const int gc = 1 << c;
-  FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
+  FT* wsf = reinterpret_cast<FT*>(reinterpret_cast<char*>(args.ws) + (long long)g * args.ws_face_stride);
   for (int idx = tid; idx < 3 * TC * TC; idx += kThreads) {
     const int fld = idx / (TC * TC), r = idx - fld * TC * TC;
     const int ii = r / TC, jj = r - ii * TC;
@@ -559,7 +560,6 @@ __device__ __forceinline__ void tile_body(const ShiftArgs& args, unsigned char* 
 // Intermediate levels ping-pong in shared memory when they fit (else through the not yet used
 // shifted-field and scratch areas of the workspace).
 constexpr int kFieldsSmem = 48 * 1024;
-template <typename FT>
 __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_constant__ ShiftArgs args) {
   extern __shared__ __align__(16) unsigned char fsmem[];
   const int g = blockIdx.x;
@@ -568,7 +568,8 @@ __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_co
   if (c == 0) return;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
-  FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
+  using FT = double;   // always fp64: the coarse recursion carries pixel-value-scale errors otherwise
+  FT* wsf = reinterpret_cast<FT*>(reinterpret_cast<char*>(args.ws) + (long long)g * args.ws_face_stride);
   const long long GC = 1ll << (2 * c);
   const bool in_smem = (15ll * (GC / 16)) * (long long)sizeof(FT) <= kFieldsSmem;   // 3 (4^(c-1) + 4^(c-2))
   FT* const bufA = in_smem ? reinterpret_cast<FT*>(fsmem) + 3 * (GC / 4) : wsf;        // level c-2, c-4, ...
@@ -646,7 +647,8 @@ __global__ void __launch_bounds__(kThreads) coarse_finish_kernel(const __grid_co
   const int c = P.m > KF ? P.m - KF : 0;
   if (c == 0) return;
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
-  FT* wsf = reinterpret_cast<FT*>(args.ws) + (long long)g * args.ws_face_stride;
+  char* wsb = reinterpret_cast<char*>(args.ws) + (long long)g * args.ws_face_stride;
+  FT* wsf = reinterpret_cast<FT*>(wsb);
   const int gc = 1 << c;
   const long long need = 3ll * gc * gc + 3ll * (gc / 2) * (gc / 2);
   if (need * (long long)sizeof(FT) <= (long long)kFinishSmem) {
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) coarse_finish_kernel(const __grid_co
     __syncthreads();
     coarse_finish<FT>(A, B0, A, c, out, args.band, false);
   } else {
-    coarse_finish<FT>(wsf, wsf + 6ll * gc * gc, wsf, c, out, args.band, true);
+    coarse_finish<FT>(wsf, reinterpret_cast<FT*>(wsb + 6ll * gc * gc * 8), wsf, c, out, args.band, true);
   }
 }
 
@@ -739,7 +741,7 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
     HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_tile_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_tile_smem<FT>()),
                   "cudaFuncSetAttribute(shift2d_tile_kernel)");
-    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_fields_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_fields_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFieldsSmem),
                   "cudaFuncSetAttribute(coarse_fields_kernel)");
     HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_finish_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -748,7 +750,7 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
     attr_done = true;
   }
   if (any_coarse) {
-    coarse_fields_kernel<FT><<<a.num_faces, kThreads, kFieldsSmem, st>>>(a);
+    coarse_fields_kernel<<<a.num_faces, kThreads, kFieldsSmem, st>>>(a);
     HS_CHECK_LAUNCH("coarse_fields_kernel");
   }
   shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);

@@ -48,9 +48,9 @@ def test_status_strings_and_version(lib):
 def test_workspace_sizes(lib):
     assert lib.haar_shift_workspace_bytes(1, 3, 1, 1) == 0
     w = lib.haar_shift_workspace_bytes(2, 8, 6, 64)
-    # per face: shifted + unshifted level-5 fields (2 * 3*4^5) + scratch 3*4^4, fp64 at N = 256
+    # per face: shifted + unshifted level-5 fields (2 * 3*4^5) + scratch 3*4^4, 8-byte slots
     assert w == 384 * (6 * 1024 + 3 * 256) * 8
-    assert lib.haar_shift_workspace_bytes(2, 7, 6, 64) == 384 * (6 * 256 + 3 * 64) * 4   # fp32 below
+    assert lib.haar_shift_workspace_bytes(2, 7, 6, 64) == 384 * (6 * 256 + 3 * 64) * 8
     assert lib.haar_shift_workspace_bytes(2, 3, 6, 64) == 0                                        # c = 0
     assert lib.haar_shift_workspace_bytes(2, 0, 1, 1) == 0
     assert lib.haar_shift_workspace_bytes(2, 13, 1, 1) == 0
