@@ -81,7 +81,10 @@ typedef enum {
  *   band_levels   0 .. log2n (log2n = full pyramid).
  *   workspace     device scratch of at least haar_shift_workspace_bytes(...) bytes (may be NULL
  *                 when that size is 0).  Contents on entry are irrelevant.
- * Result: out = S_s in, equal (to fp32 rounding) to forward(box_shift(inverse(in))).
+ * Result: out = S_s in, equal to forward(box_shift(inverse(in))) within fp32 output rounding:
+ * the difference fields are carried in fp64 for N >= 256 (and always for the coarse levels
+ * above the tiles) because fp32 field rounding is amplified ~2^(n-l) on the coarse outputs
+ * (DESIGN.md §4.1).
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, int faces,
                             int batch, const double* shifts_host, int band_levels,
@@ -133,9 +136,10 @@ HS_API size_t haar_shift_coarse_workspace_bytes(int in_log2n, int start_level, i
  *                 1024-byte aligned (may be NULL when that size is 0).
  * Accumulation is fp32.  batch <= 8: CUDA-core streaming GEMV.  batch a multiple of 64 with
  * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16 (T and the
- * per-frame-scaled light each split into fp16 hi + lo, three products, fp32 accumulation in TMEM;
- * ~2^-21 relative per product; requires |T| < 2^15 -- transfer coefficients of an orthonormal
- * basis are bounded by the function's L2 norm).  Other batches: CUDA-core tiled GEMM.
+ * per-frame-scaled light each split into fp16 hi + lo, three products, fp32 accumulation in TMEM
+ * drained into fp32 registers every 1024 k; ~2^-21 relative per product; requires |T| < 2^15 --
+ * transfer coefficients of an orthonormal basis are bounded by the function's L2 norm).  Other
+ * batches: CUDA-core tiled GEMM.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
                            const float* light, int64_t light_face_stride, int batch,
