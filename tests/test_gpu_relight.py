@@ -53,7 +53,7 @@ def test_strided_light_band_from_full_pyramids():
     assert _rel(R.cpu().numpy(), orelight.relight(T, L, faces, kf)) <= TOL
 
 
-@pytest.mark.parametrize("B", [9, 13, 64, 128])
+@pytest.mark.parametrize("B", [9, 13, 64, 128, 1024])
 def test_gemm_batches(B):
     import torch
     import paper_1705_07272_b200 as hs

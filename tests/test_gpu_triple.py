@@ -106,7 +106,7 @@ def _run(k, faces, V, B, light_log2n=None, seed=50):
 
 
 @pytest.mark.parametrize("k,faces,V,B", [(3, 1, 257, 64), (4, 6, 300, 64), (5, 6, 1000, 64), (5, 6, 333, 128),
-                                         (6, 1, 200, 64), (5, 1, 1, 64)])
+                                         (6, 1, 200, 64), (5, 1, 1, 64), (4, 2, 150, 1024)])
 def test_triple_tensor_core_parity(k, faces, V, B):
     got, ref = _run(k, faces, V, B)
     assert _rel(got, ref) <= TOL
