@@ -82,9 +82,8 @@ typedef enum {
  *   workspace     device scratch of at least haar_shift_workspace_bytes(...) bytes (may be NULL
  *                 when that size is 0).  Contents on entry are irrelevant.
  * Result: out = S_s in, equal to forward(box_shift(inverse(in))) within fp32 output rounding:
- * the difference fields are carried in fp64 for N >= 256 (and always for the coarse levels
- * above the tiles) because fp32 field rounding is amplified ~2^(n-l) on the coarse outputs
- * (DESIGN.md §4.1).
+ * the 2D difference fields are carried in fp64 at every size because fp32 field rounding is
+ * amplified ~2^(n-l) on the coarse outputs.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, int faces,
                             int batch, const double* shifts_host, int band_levels,

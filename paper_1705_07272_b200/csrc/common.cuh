@@ -125,7 +125,6 @@ constexpr int kTileKF = 3;    // fine levels per tile: the tile root level is c 
 constexpr int kTileTC = 8;    // tile side at level c (cells)
 
 inline int coarse_level(int m) { return m > kTileKF ? m - kTileKF : 0; }
-bool shift2d_uses_fp64(int log2n);        // field precision of the 2D tile kernel
 inline long long ws_face_floats_2d(int n) {  // 8-byte elements per face
   // [shifted level-c fields 3*4^c (tile field type)][unshifted level-c fields 3*4^c (fp64)]
   // [scratch 3*4^(c-1)]

@@ -21,8 +21,11 @@ constexpr int k1DThreads = 256;
 //   Delta_l[k] = a_l[k] - a_l[k+1]; top-down Delta_{l+1}[2k] = 2 d^_l[k],
 //   Delta_{l+1}[2k+1] = Delta_l[k] - d^_l[k] - d^_l[k+1]; shift at level m;
 //   bottom-up d^'_l[k] = Delta'_{l+1}[2k] / 2, Delta'_l[k] = (D'[2k] + 2 D'[2k+1] + D'[2k+2]) / 2.
+// The differences are carried in fp64 (one rounding per output): fp32 rounding of the fine
+// differences is amplified ~2^(n-l) on a coarse band (1.2e-5 measured for white
+// noise at N = 2048-4096 in fp32).
 __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_constant__ ShiftArgs args) {
-  extern __shared__ __align__(16) float smem[];
+  extern __shared__ __align__(16) double smem[];
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int n = args.log2n, N = 1 << n;
@@ -32,8 +35,8 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const int band = args.band;
   const int Kb = 1 << band;
-  float* d0 = smem;      // N floats: Delta at the current level
-  float* d1 = smem + N;  // N floats
+  double* d0 = smem;      // N doubles: Delta at the current level
+  double* d1 = smem + N;  // N doubles
   // levels >= m: permutation by q / 2^(n-l); scaling copied
   for (int idx = threadIdx.x; idx < Kb; idx += blockDim.x) {
     if (idx == 0) {
@@ -48,45 +51,45 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
   }
   if (m == 0) return;
   // top-down Delta_1 .. Delta_m  (Delta_0 = 0)
-  float* cur = d0;
-  float* nxt = d1;
-  if (threadIdx.x == 0) cur[0] = 0.f;
+  double* cur = d0;
+  double* nxt = d1;
+  if (threadIdx.x == 0) cur[0] = 0.0;
   __syncthreads();
   for (int l = 0; l < m; ++l) {
     const int gl = 1 << l;
-    const float asc = exp2f((float)l * 0.5f);  // unit-interval -> averaging: x 2^(l/2)
+    const double asc = exp2((double)l * 0.5);  // unit-interval -> averaging: x 2^(l/2)
     for (int kk = threadIdx.x; kk < gl; kk += blockDim.x) {
-      const float dk = in[gl + kk] * asc;
-      const float dk1 = in[gl + ((kk + 1) & (gl - 1))] * asc;
-      nxt[2 * kk] = 2.f * dk;
+      const double dk = (double)in[gl + kk] * asc;
+      const double dk1 = (double)in[gl + ((kk + 1) & (gl - 1))] * asc;
+      nxt[2 * kk] = 2.0 * dk;
       nxt[2 * kk + 1] = cur[kk] - dk - dk1;
     }
     __syncthreads();
-    float* t = cur;
+    double* t = cur;
     cur = nxt;
     nxt = t;
   }
   // shift at level m, then bottom-up m-1 .. 0
   const int gm = 1 << m;
-  const float w0 = 1.f - P.wx, w1 = P.wx;
+  const double w0 = 1.0 - (double)P.wx, w1 = (double)P.wx;
   for (int x = threadIdx.x; x < gm; x += blockDim.x)
     nxt[x] = w0 * cur[(x - P.Qx) & (gm - 1)] + w1 * cur[(x - P.Qx - 1) & (gm - 1)];
   __syncthreads();
   {
-    float* t = cur;
+    double* t = cur;
     cur = nxt;
     nxt = t;
   }
   for (int l = m - 1; l >= 0; --l) {
     const int gl = 1 << l, G = 2 * gl;
-    const float osc = exp2f(-(float)l * 0.5f);
+    const double osc = exp2(-(double)l * 0.5);
     for (int kk = threadIdx.x; kk < gl; kk += blockDim.x) {
-      const float a0 = cur[2 * kk], a1 = cur[2 * kk + 1], a2 = cur[(2 * kk + 2) & (G - 1)];
-      nxt[kk] = 0.5f * (a0 + 2.f * a1 + a2);
-      if (l < band) out[gl + kk] = 0.5f * a0 * osc;
+      const double a0 = cur[2 * kk], a1 = cur[2 * kk + 1], a2 = cur[(2 * kk + 2) & (G - 1)];
+      nxt[kk] = 0.5 * (a0 + 2.0 * a1 + a2);
+      if (l < band) out[gl + kk] = (float)(0.5 * a0 * osc);
     }
     __syncthreads();
-    float* t = cur;
+    double* t = cur;
     cur = nxt;
     nxt = t;
   }
@@ -164,7 +167,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
       hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, st);
       if (s != HS_OK) return s;
     } else {
-      const size_t smem = (size_t)2 * (1u << n) * sizeof(float);
+      const size_t smem = (size_t)2 * (1u << n) * sizeof(double);
       if (smem > 48 * 1024) {
         HS_CHECK_CUDA(cudaFuncSetAttribute(shift1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem),
