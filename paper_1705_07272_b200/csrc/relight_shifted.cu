@@ -438,6 +438,7 @@ __device__ __forceinline__ void unit_body2(const float* plane, float* scratch, u
   constexpr int N = Gm::N, G = Gm::G, RS = Gm::RS, QPP = Gm::QPP, PLANE = Gm::PLANE, SPLIT = Gm::SPLIT;
   constexpr int n = LOG2N;
   static_assert(Gm::CPT == 2 && G == 64 && Gm::TPR == 32, "a warp holds one level n-1 row");
+  static_assert(1 + 2 * VG <= 16, "named barriers");
   constexpr int NTK = (FLD == 1) ? 5 : 6;
   const int grp = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
   const int bar = 1 + grp;
@@ -473,7 +474,8 @@ __device__ __forceinline__ void unit_body2(const float* plane, float* scratch, u
   uint32_t phases = 0;   // bit b: parity of buffer b
   int b = 0;
   int4 pr_next = (v0 + grp < v1) ? __ldg(vparams + v0 + grp) : make_int4(0, 0, 0, 0);
-  for (long long v = v0 + grp; v < v1; v += VG, b ^= 1) {
+  int it = 0;   // vertex iteration of this group
+  for (long long v = v0 + grp; v < v1; v += VG, b ^= 1, ++it) {
     const int4 pr = pr_next;   // loaded one vertex ahead (its latency was on the critical path)
     if (v + VG < v1) pr_next = __ldg(vparams + v + VG);
     const float* Tv = T + v * Kt + (long long)f * NN;
@@ -482,7 +484,7 @@ __device__ __forceinline__ void unit_body2(const float* plane, float* scratch, u
     // coarse-level T values, in flight during the stencil: level n-3 (one cell per thread) and,
     // for the warp that runs levels 3 .. 0 of this vertex (rotating, so no warp lags), those
     static_assert(LOG2N - 3 == 4, "level n-3 is the last group-wide level");
-    const int wl = (int)(((v - v0 - grp) / VG) & 7);
+    const int wl = it & 7;
     const float t3 = __ldg(Tv + ((long long)(1 + FLD) << (2 * (n - 3))) + tid);
     float tw[5];
     if (warp == wl) {
@@ -588,11 +590,14 @@ __device__ __forceinline__ void unit_body2(const float* plane, float* scratch, u
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     float* rd = red + 8 * b;
     if (lane == 0) rd[warp] = acc;
+    // a barrier of its own (ids 1 + VG ..): a warp that arrives here and runs ahead reaches the
+    // group barrier of the next vertex before this one has necessarily completed
+    const int bar2 = 1 + VG + grp;
     if (warp != wl) {
-      group_arrive(bar);   // S3 and this warp's partial are published; go on to the next vertex
+      group_arrive(bar2);   // S3 and this warp's partial are published; go on to the next vertex
       continue;
     }
-    group_sync(bar);
+    group_sync(bar2);
     // levels 3 .. 0 on warp wl (warp-synchronous), then the fixed-order sum of the partials
     float aw = 0.f;
     {
