@@ -41,9 +41,9 @@ namespace {
 constexpr int kRotChunk = 1024;   // maps per launch sequence (angles travel as kernel parameters)
 constexpr int kDcLevel = 6;
 
-struct RotParams {
-  float ca[kRotChunk];
-  float sa[kRotChunk];
+struct RotParams {   // kernel parameter space holds up to 32 KB: 2 x 1024 doubles
+  double ca[kRotChunk];
+  double sa[kRotChunk];
 };
 
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
@@ -98,38 +98,75 @@ __global__ void rot_topdown_kernel(const float* __restrict__ in, long long maps,
 
 // ------------------------------------------------------------------------------- (2) chain rule
 // (Theta, Phi) of R_x(alpha) p(theta, phi): eq:theta / eq:phi, Phi in [0, 2 pi)
+// The angle arithmetic runs in fp64: the chain rule takes differences of nearby rotated angles
+// (dTheta, dPhi ~ pi / N), which fp32 resolves to only ~1e-5 relative at N = 128.
 struct Ang {
-  float Th, Ph;
+  double Th, Ph;
 };
 
-__device__ __forceinline__ Ang rotated(float th, float ph, float ca, float sa) {
-  float st, ct, sp, cp;
-  sincosf(th, &st, &ct);
-  sincosf(ph, &sp, &cp);
-  const float a = st * sp;                   // x' = x
-  const float u = ca * ct - sa * st * cp;    // y' = cos Theta
-  const float b = sa * ct + ca * st * cp;    // z'
+// sin / cos of the half-step grid angles: theta = k pi / (2N), phi = k pi / N, k = 0 .. 2N+1
+// (every sample of the chain rule -- pixel centres, neighbours, midpoints -- is on this grid)
+struct Trig {
+  const double* sT;
+  const double* cT;
+  const double* sP;
+  const double* cP;
+};
+
+__global__ void rot_table_kernel(int n, double* __restrict__ tab) {
+  const int N = 1 << n, K = 2 * N + 2;
+  for (int k = threadIdx.x + blockIdx.x * blockDim.x; k < K; k += blockDim.x * gridDim.x) {
+    double s, c;
+    sincospi((double)k / (2.0 * N), &s, &c);
+    tab[k] = s;
+    tab[K + k] = c;
+    sincospi((double)k / (double)N, &s, &c);
+    tab[2 * K + k] = s;
+    tab[3 * K + k] = c;
+  }
+}
+
+// rotated angles of the grid point (theta, phi) = (kt pi / 2N, kp pi / N)
+__device__ __forceinline__ Ang rotated_k(const Trig& tr, int kt, int kp, double ca, double sa) {
+  const double st = __ldg(tr.sT + kt), ct = __ldg(tr.cT + kt), sp = __ldg(tr.sP + kp), cp = __ldg(tr.cP + kp);
+  const double a = st * sp;
+  const double u = ca * ct - sa * st * cp;
+  const double b = sa * ct + ca * st * cp;
   Ang r;
-  r.Th = acosf(fminf(1.f, fmaxf(-1.f, u)));
-  float P = atan2f(a, b);
-  if (P < 0.f) P += 6.283185307179586f;
+  r.Th = acos(fmin(1.0, fmax(-1.0, u)));
+  double P = atan2(a, b);
+  if (P < 0.0) P += 6.283185307179586;
   r.Ph = P;
   return r;
 }
 
+// the same in fp32 for the DC's sample points (a mean over N^2 samples of a level-6 approximation;
+// the chain rule's midpoints need fp64: an fp32 position moves a white-noise field sample by ~1e-5)
+__device__ __forceinline__ void rotated_kf(const Trig& tr, int kt, int kp, float ca, float sa, float& Th, float& Ph) {
+  const float st = (float)__ldg(tr.sT + kt), ct = (float)__ldg(tr.cT + kt), sp = (float)__ldg(tr.sP + kp),
+              cp = (float)__ldg(tr.cP + kp);
+  const float a = st * sp;
+  const float u = ca * ct - sa * st * cp;
+  const float b = sa * ct + ca * st * cp;
+  Th = acosf(fminf(1.f, fmaxf(-1.f, u)));
+  float P = atan2f(a, b);
+  if (P < 0.f) P += 6.283185307179586f;
+  Ph = P;
+}
+
 // bilinear sample of a field plane (rows 0..R-1) extended by the reflected rows lo (row -1) and
 // hi (row R) at index coordinates (y, x), periodic in x
-__device__ __forceinline__ float sample_ext(const float* __restrict__ P, const float* __restrict__ lo,
-                                           const float* __restrict__ hi, int N, int R, float y, float x) {
-  y = fminf(fmaxf(y, -1.f), (float)R);
-  const float fy = floorf(y), fx = floorf(x);
-  const float wy = y - fy, wx = x - fx;
+__device__ __forceinline__ double sample_ext(const float* __restrict__ P, const float* __restrict__ lo,
+                                            const float* __restrict__ hi, int N, int R, double y, double x) {
+  y = fmin(fmax(y, -1.0), (double)R);
+  const double fy = floor(y), fx = floor(x);
+  const double wy = y - fy, wx = x - fx;
   const int y0 = (int)fy, y1 = min(y0 + 1, R);
   const int x0 = ((int)fx) & (N - 1), x1 = (x0 + 1) & (N - 1);
   const float* r0 = y0 < 0 ? lo : (y0 >= R ? hi : P + y0 * N);
   const float* r1 = y1 < 0 ? lo : (y1 >= R ? hi : P + y1 * N);
-  return (1.f - wy) * ((1.f - wx) * __ldg(r0 + x0) + wx * __ldg(r0 + x1)) +
-         wy * ((1.f - wx) * __ldg(r1 + x0) + wx * __ldg(r1 + x1));
+  return (1.0 - wy) * ((1.0 - wx) * (double)__ldg(r0 + x0) + wx * (double)__ldg(r0 + x1)) +
+         wy * ((1.0 - wx) * (double)__ldg(r1 + x0) + wx * (double)__ldg(r1 + x1));
 }
 
 // pole rows per map: E [map][4][N] = X row -1, X row N, Y row -1, Y row N-1 (reflected)
@@ -153,35 +190,35 @@ __global__ void rot_pole_kernel(const float* __restrict__ F, int n, float* __res
 
 // f's fields F [map][2][N][N] (X_f, Y_f) + pole rows E; g's fields out: G [map][2][N][N]
 __global__ void rot_chainrule_kernel(const float* __restrict__ F, const float* __restrict__ E, long long maps, int n,
-                                     const __grid_constant__ RotParams prm, float* __restrict__ Gf) {
+                                     const __grid_constant__ RotParams prm, Trig tr, float* __restrict__ Gf) {
   const int N = 1 << n;
   const long long NN = 1ll << (2 * n);
   const long long total = maps * NN;
-  const float kT = 3.14159265358979f / (float)N, kP = 6.283185307179586f / (float)N;
-  const float iT = (float)N / 3.14159265358979f, iP = (float)N / 6.283185307179586f;
+  const double iT = (double)N / 3.141592653589793, iP = (double)N / 6.283185307179586;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long b = e >> (2 * n);
     const int pix = (int)(e & (NN - 1));
     const int i = pix >> n, j = pix & (N - 1);
-    const float ca = prm.ca[b], sa = prm.sa[b];
+    const double ca = prm.ca[b], sa = prm.sa[b];
     const float* Xf = F + b * 2 * NN;
     const float* Yf = Xf + NN;
     const float* Eb = E + b * 4 * N;
-    const Ang A0 = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
+    // half-step grid indices: pixel centre (2i+1, 2j+1), neighbour +2, midpoint +1
+    const Ang A0 = rotated_k(tr, 2 * i + 1, 2 * j + 1, ca, sa);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
-      const float di = t ? 1.f : 0.f, dj = t ? 0.f : 1.f;
-      const Ang A1 = rotated(((float)i + 0.5f + di) * kT, ((float)j + 0.5f + dj) * kP, ca, sa);
-      const Ang M = rotated(((float)i + 0.5f + 0.5f * di) * kT, ((float)j + 0.5f + 0.5f * dj) * kP, ca, sa);
-      const float y = M.Th * iT - 0.5f, x = M.Ph * iP - 0.5f;
-      const float xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5f);           // X_f lives at (i, j + 1/2)
-      const float yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5f, x);  // Y_f at (i + 1/2, j)
-      const float dT = A0.Th - A1.Th;
-      float dP = A0.Ph - A1.Ph;
-      if (dP > 3.14159265358979f) dP -= 6.283185307179586f;
-      if (dP < -3.14159265358979f) dP += 6.283185307179586f;
-      Gf[b * 2 * NN + t * NN + pix] = -yf * dT * iT - xf * dP * iP;
+      const int di = t, dj = 1 - t;
+      const Ang A1 = rotated_k(tr, 2 * i + 1 + 2 * di, 2 * j + 1 + 2 * dj, ca, sa);
+      const Ang M = rotated_k(tr, 2 * i + 1 + di, 2 * j + 1 + dj, ca, sa);
+      const double y = M.Th * iT - 0.5, x = M.Ph * iP - 0.5;
+      const double xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5);           // X_f lives at (i, j + 1/2)
+      const double yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5, x);  // Y_f at (i + 1/2, j)
+      const double dT = A0.Th - A1.Th;
+      double dP = A0.Ph - A1.Ph;
+      if (dP > 3.141592653589793) dP -= 6.283185307179586;
+      if (dP < -3.141592653589793) dP += 6.283185307179586;
+      Gf[b * 2 * NN + t * NN + pix] = (float)(-yf * dT * iT - xf * dP * iP);
     }
   }
 }
@@ -251,7 +288,8 @@ __global__ void rot_bottomup_kernel(const float* __restrict__ src, int src_plane
 
 // ------------------------------------------------------------------------------- scaling
 __global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ in, int n, long long map0,
-                                                     const __grid_constant__ RotParams prm, float* __restrict__ out) {
+                                                     const __grid_constant__ RotParams prm, Trig tr,
+                                                     float* __restrict__ out) {
   __shared__ float A[2][1 << (2 * kDcLevel)];
   __shared__ float red[8];
   const long long b = blockIdx.x;
@@ -280,14 +318,14 @@ __global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ i
   }
   const int M = 1 << L;
   const int N = 1 << n;
-  const float ca = prm.ca[map0 + b], sa = prm.sa[map0 + b];
-  const float kT = 3.14159265358979f / (float)N, kP = 6.283185307179586f / (float)N;
+  const double ca = prm.ca[map0 + b], sa = prm.sa[map0 + b];
   float acc = 0.f;
   for (long long p = threadIdx.x; p < NN; p += blockDim.x) {
     const int i = (int)(p >> n), j = (int)(p & (N - 1));
-    const Ang J = rotated(((float)i + 0.5f) * kT, ((float)j + 0.5f) * kP, ca, sa);
-    const float y = J.Th * (float)M / 3.14159265358979f - 0.5f;   // in [-1/2, M - 1/2]
-    const float x = J.Ph * (float)M / 6.283185307179586f - 0.5f;
+    float jT, jP;
+    rotated_kf(tr, 2 * i + 1, 2 * j + 1, (float)ca, (float)sa, jT, jP);
+    const float y = jT * (float)M / 3.14159265358979f - 0.5f;   // in [-1/2, M - 1/2]
+    const float x = jP * (float)M / 6.283185307179586f - 0.5f;
     const float fy = floorf(y), fx = floorf(x);
     const float wy = y - fy, wx = x - fx;
     const float* P = A[cb];
@@ -325,7 +363,8 @@ size_t rotate_workspace_bytes_impl(int log2n, long long maps) {
   const size_t NN = (size_t)1 << (2 * log2n);
   const size_t f = (size_t)maps * NN * sizeof(float);
   const size_t pb = ((size_t)maps * 4 * ((size_t)1 << log2n) * sizeof(float) + 255) & ~size_t(255);
-  return 2 * 2 * f + 2 * f + f + pb + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
+  const size_t tb = (4 * (2 * ((size_t)1 << log2n) + 2) * sizeof(double) + 255) & ~size_t(255);
+  return 2 * 2 * f + 2 * f + f + pb + tb + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
 }
 
 hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
@@ -339,15 +378,21 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
   float* tmp = reinterpret_cast<float*>(base + 6 * f);
   const size_t pb = ((size_t)maps * 4 * ((size_t)1 << n) * sizeof(float) + 255) & ~size_t(255);
   float* poles = reinterpret_cast<float*>(base + 7 * f);
-  void* sws = base + 7 * f + pb;
-  const size_t sws_bytes = ws_bytes - 7 * f - pb;
+  const int K = 2 * (1 << n) + 2;
+  const size_t tb = (4 * (size_t)K * sizeof(double) + 255) & ~size_t(255);
+  double* tab = reinterpret_cast<double*>(base + 7 * f + pb);
+  void* sws = base + 7 * f + pb + tb;
+  const size_t sws_bytes = ws_bytes - 7 * f - pb - tb;
+  rot_table_kernel<<<(K + 255) / 256, 256, 0, st>>>(n, tab);
+  HS_CHECK_LAUNCH("rot_table_kernel");
+  const Trig tr{tab, tab + K, tab + 2 * K, tab + 3 * K};
 
   for (long long m0 = 0; m0 < maps; m0 += kRotChunk) {
     const long long mc = (maps - m0) < kRotChunk ? (maps - m0) : kRotChunk;
     RotParams prm;
     for (long long k = 0; k < mc; ++k) {
-      prm.ca[k] = (float)std::cos(angles[2 * (m0 + k)]);
-      prm.sa[k] = (float)std::sin(angles[2 * (m0 + k)]);
+      prm.ca[k] = std::cos(angles[2 * (m0 + k)]);
+      prm.sa[k] = std::sin(angles[2 * (m0 + k)]);
     }
     const float* src = in + m0 * NN;
     float* dtmp = tmp + m0 * NN;
@@ -362,7 +407,7 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
     // (2) pole rows, chain rule, closure
     rot_pole_kernel<<<(unsigned)mc, 256, 0, st>>>(cur, n, poles);
     HS_CHECK_LAUNCH("rot_pole_kernel");
-    rot_chainrule_kernel<<<grid_for(mc * NN), 256, 0, st>>>(cur, poles, mc, n, prm, Gf);
+    rot_chainrule_kernel<<<grid_for(mc * NN), 256, 0, st>>>(cur, poles, mc, n, prm, tr, Gf);
     HS_CHECK_LAUNCH("rot_chainrule_kernel");
     rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
     HS_CHECK_LAUNCH("rot_closure_kernel");
@@ -377,7 +422,7 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
       planes = 3;
       d = (d == bufA) ? bufB : bufA;
     }
-    rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, n, 0, prm, dtmp);
+    rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, n, 0, prm, tr, dtmp);
     HS_CHECK_LAUNCH("rot_dc_kernel");
   }
   // azimuth: the exact shift by beta N / (2 pi) columns
