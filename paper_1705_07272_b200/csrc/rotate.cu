@@ -188,38 +188,49 @@ __global__ void rot_pole_kernel(const float* __restrict__ F, int n, float* __res
   }
 }
 
-// f's fields F [map][2][N][N] (X_f, Y_f) + pole rows E; g's fields out: G [map][2][N][N]
-__global__ void rot_chainrule_kernel(const float* __restrict__ F, const float* __restrict__ E, long long maps, int n,
-                                     const __grid_constant__ RotParams prm, Trig tr, float* __restrict__ Gf) {
+// f's fields F [map][2][N][N] (X_f, Y_f) + pole rows E; g's fields out: G [map][2][N][N].
+// One CTA per TS x TS pixel tile of one map: the rotated pixel centres of the tile and its
+// +1 halo (row and column) are computed once into shared memory, so each pixel costs three fp64
+// rotations (its centre, shared with two neighbours' differences, and two midpoints) instead of five.
+constexpr int kTS = 16;
+__global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const float* __restrict__ F, const float* __restrict__ E,
+                                                                  int n, const __grid_constant__ RotParams prm, Trig tr,
+                                                                  float* __restrict__ Gf) {
+  __shared__ Ang C[kTS + 1][kTS + 1];
   const int N = 1 << n;
+  const int TS = N < kTS ? N : kTS;
+  const int tpr = N / TS;                         // tiles per row of the map
   const long long NN = 1ll << (2 * n);
-  const long long total = maps * NN;
+  const int b = blockIdx.y;
+  const int i0 = (blockIdx.x / tpr) * TS, j0 = (blockIdx.x % tpr) * TS;
+  const double ca = prm.ca[b], sa = prm.sa[b];
+  const int nt = TS * TS;
+  for (int k = threadIdx.x; k < (TS + 1) * (TS + 1); k += nt) {
+    const int r = k / (TS + 1), c = k - r * (TS + 1);
+    C[r][c] = rotated_k(tr, 2 * (i0 + r) + 1, 2 * (j0 + c) + 1, ca, sa);   // row / column N: beyond pole / 2 pi
+  }
+  __syncthreads();
+  if (threadIdx.x >= nt) return;
+  const int ti = threadIdx.x / TS, tj = threadIdx.x - ti * TS;
+  const int i = i0 + ti, j = j0 + tj;
   const double iT = (double)N / 3.141592653589793, iP = (double)N / 6.283185307179586;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long b = e >> (2 * n);
-    const int pix = (int)(e & (NN - 1));
-    const int i = pix >> n, j = pix & (N - 1);
-    const double ca = prm.ca[b], sa = prm.sa[b];
-    const float* Xf = F + b * 2 * NN;
-    const float* Yf = Xf + NN;
-    const float* Eb = E + b * 4 * N;
-    // half-step grid indices: pixel centre (2i+1, 2j+1), neighbour +2, midpoint +1
-    const Ang A0 = rotated_k(tr, 2 * i + 1, 2 * j + 1, ca, sa);
+  const float* Xf = F + (long long)b * 2 * NN;
+  const float* Yf = Xf + NN;
+  const float* Eb = E + (long long)b * 4 * N;
+  const Ang A0 = C[ti][tj];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
-      const int di = t, dj = 1 - t;
-      const Ang A1 = rotated_k(tr, 2 * i + 1 + 2 * di, 2 * j + 1 + 2 * dj, ca, sa);
-      const Ang M = rotated_k(tr, 2 * i + 1 + di, 2 * j + 1 + dj, ca, sa);
-      const double y = M.Th * iT - 0.5, x = M.Ph * iP - 0.5;
-      const double xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5);           // X_f lives at (i, j + 1/2)
-      const double yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5, x);  // Y_f at (i + 1/2, j)
-      const double dT = A0.Th - A1.Th;
-      double dP = A0.Ph - A1.Ph;
-      if (dP > 3.141592653589793) dP -= 6.283185307179586;
-      if (dP < -3.141592653589793) dP += 6.283185307179586;
-      Gf[b * 2 * NN + t * NN + pix] = (float)(-yf * dT * iT - xf * dP * iP);
-    }
+  for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
+    const int di = t, dj = 1 - t;
+    const Ang A1 = C[ti + di][tj + dj];
+    const Ang M = rotated_k(tr, 2 * i + 1 + di, 2 * j + 1 + dj, ca, sa);   // midpoint (half-step grid)
+    const double y = M.Th * iT - 0.5, x = M.Ph * iP - 0.5;
+    const double xf = sample_ext(Xf, Eb, Eb + N, N, N, y, x - 0.5);           // X_f lives at (i, j + 1/2)
+    const double yf = sample_ext(Yf, Eb + 2 * N, Eb + 3 * N, N, N - 1, y - 0.5, x);  // Y_f at (i + 1/2, j)
+    const double dT = A0.Th - A1.Th;
+    double dP = A0.Ph - A1.Ph;
+    if (dP > 3.141592653589793) dP -= 6.283185307179586;
+    if (dP < -3.141592653589793) dP += 6.283185307179586;
+    Gf[(long long)b * 2 * NN + t * NN + (long long)i * N + j] = (float)(-yf * dT * iT - xf * dP * iP);
   }
 }
 
@@ -407,7 +418,12 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
     // (2) pole rows, chain rule, closure
     rot_pole_kernel<<<(unsigned)mc, 256, 0, st>>>(cur, n, poles);
     HS_CHECK_LAUNCH("rot_pole_kernel");
-    rot_chainrule_kernel<<<grid_for(mc * NN), 256, 0, st>>>(cur, poles, mc, n, prm, tr, Gf);
+    {
+      const int TS = (1 << n) < kTS ? (1 << n) : kTS;
+      const int tiles = (int)(NN / ((long long)TS * TS));
+      const int thr = (TS + 1) * (TS + 1) > TS * TS ? ((TS * TS + 31) / 32) * 32 : TS * TS;
+      rot_chainrule_kernel<<<dim3(tiles, (unsigned)mc), thr < 32 ? 32 : thr, 0, st>>>(cur, poles, n, prm, tr, Gf);
+    }
     HS_CHECK_LAUNCH("rot_chainrule_kernel");
     rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
     HS_CHECK_LAUNCH("rot_closure_kernel");
