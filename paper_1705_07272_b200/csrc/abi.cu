@@ -363,6 +363,7 @@ hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_t row_s
   if (!indices || !values || row_start < 0 || row_count < 1 || faces < 1) return HS_ERR_INVALID_ARG;
   if (log2n < 1 || log2n > HS_MAX_LOG2N || dense_levels < 0 || dense_levels > log2n) return HS_ERR_INVALID_ARG;
   if (k_sparse < (faces << (2 * dense_levels)) || (long long)faces << (2 * log2n) >= (1ll << 31)) return HS_ERR_INVALID_ARG;
+  if (k_sparse > (faces << (2 * dense_levels)) && dense_levels >= log2n) return HS_ERR_INVALID_ARG;   // no level to draw
   if (!aligned16(indices) || !aligned16(values)) return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
   if (s != HS_OK) return s;

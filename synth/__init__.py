@@ -135,6 +135,8 @@ def sparse_transfer_rows(seed: int, row_start: int, row_count: int, faces: int, 
     nd = faces * 4 ** dense_levels
     if k_sparse < nd:
         raise ValueError("k_sparse must cover the dense coarse levels")
+    if k_sparse > nd and dense_levels >= log2n:
+        raise ValueError("no detail level left to draw the sparse entries from (dense_levels >= log2n)")
     v = np.arange(row_start, row_start + row_count, dtype=np.uint64)[:, None]
     k = np.arange(k_sparse, dtype=np.uint64)[None, :]
     gi = v * np.uint64(k_sparse) + k

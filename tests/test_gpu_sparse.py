@@ -53,3 +53,19 @@ def test_sparse_relight_after_shift_c5_shape_subset():
     torch.cuda.synchronize()
     ref = orelight.relight_sparse(idx.cpu().numpy(), val.cpu().numpy(), shifted.cpu().numpy().reshape(B, -1))
     assert np.linalg.norm(R.cpu().numpy() - ref) / np.linalg.norm(ref) <= TOL
+
+
+@pytest.mark.parametrize("faces,n,B,ks", [(6, 6, 64, 150), (6, 2, 3, 150), (24, 4, 70, 152), (1, 8, 128, 256),
+                                          (2, 5, 64, 33)])
+def test_sparse_shapes(faces, n, B, ks):
+    """full 64-frame blocks (vectorised path: K_s % 4 == 0) and ragged ones (scalar path), one and
+    many faces, B = 70 mixing both"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    V = 555
+    idx, val = synth.sparse_transfer_rows(80, 0, V, faces, n, ks, 1 if faces > 6 else min(2, n - 1))
+    light = synth.light_pyramids(81, B, faces, n)
+    R = hs.relight_vertices_sparse(torch.from_numpy(idx).cuda(), torch.from_numpy(val).cuda(),
+                                   torch.from_numpy(light).cuda()).cpu().numpy()
+    ref = orelight.relight_sparse(idx, val, light.reshape(B, -1))
+    assert np.linalg.norm(R - ref) / np.linalg.norm(ref) <= TOL
