@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) relight_sparse64_kernel(const int* __rest
     const int4* iv = reinterpret_cast<const int4*>(idx + v * ks);
     const float4* vv = reinterpret_cast<const float4*>(val + v * ks);
     float a0 = 0.f, a1 = 0.f;
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < ks / 4; ++k) {
       const int4 i = __ldg(iv + k);
       const float4 w = __ldg(vv + k);
