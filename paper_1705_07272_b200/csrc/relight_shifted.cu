@@ -18,8 +18,6 @@
 // Every shift is processed at the finest level (integer shifts have phi = 0), which is exact.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace hs {
@@ -731,9 +729,8 @@ hs_status launch_unit_vg(const float* T, long long V, int faces, const float* fi
 template <int LOG2N>
 hs_status launch_unit(const float* T, long long V, int faces, const float* fields, const int4* shifts,
                       float* partial, cudaStream_t st) {
-  static int vg = [] { const char* e = getenv("HS_C4_VG"); return e ? atoi(e) : kVG; }();
-  if (vg == 2) return launch_unit_vg<LOG2N, 2>(T, V, faces, fields, shifts, partial, st);
-  if (vg == 4 && Geo<LOG2N>::smem(4) <= 227 * 1024) return launch_unit_vg<LOG2N, (Geo<LOG2N>::smem(4) <= 227 * 1024 ? 4 : 3)>(T, V, faces, fields, shifts, partial, st);
+  // three groups: measured 12.5 ms at c4 against 16.5 ms with two (fewer warps to cover the
+  // group barriers); four do not fit the N = 128 scratch
   return launch_unit_vg<LOG2N, kVG>(T, V, faces, fields, shifts, partial, st);
 }
 
