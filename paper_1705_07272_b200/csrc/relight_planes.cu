@@ -1,0 +1,388 @@
+// Fused per-vertex shift + relight at N = 128 by residue planes (DESIGN.md
+// §5.5).  r_v = < S_{s_v} L , T_v >.
+//
+// The shift of a difference field F at the finest level is the box projection
+//   S F = sum_{a,b in {0,1}} w^y_a w^x_b roll(F, (q_y + a, q_x + b)),   w_0 = 1 - phi, w_1 = phi,
+// and the bottom-up BU (the paper's [1,1] x [1,2,1] recursion) is linear and
+// commutes with rolls by even amounts:  BU(roll(X, 2R)) = roll(BU(X), R).  Hence for Q = q + (a, b)
+//   BU^k(roll(F, Q)) = roll(P_{k, Q mod 2^k}, Q div 2^k),   P_{k, rho} = BU(roll(P_{k-1, rho mod 2^(k-1)},
+//                                                                     rho div 2^(k-1)))
+// -- a light-only precomputation over the 4^k residues rho.  Per vertex, the level n-1 and n-2
+// outputs are then four rolled reads of precomputed planes instead of a shift + stencil:
+//   planes_kernel   (per face and field, fp64): D1[4][64][64] (level n-1 details), D2[16][32][32]
+//                   (level n-2 details), F2[16][32][32] (level n-2 fields), scales folded in;
+//   planes3_kernel  DF3[64][16][16] (level n-3 (detail, field) pairs) from F2;
+//   planes_a_kernel one warp per vertex: sum_ab w_ab (< T_{n-1}, roll(D1_ab) > + < T_{n-2}, roll(D2_ab) >)
+//                   (D1 rows doubled in shared memory so a warp's 64 rows never wrap; HBM-bound);
+//   planes_c_kernel one warp per vertex: level n-3 details and field from DF3 the same way, then the
+//                   bottom-up 3 .. 0 warp-synchronously (T: 1.4 KB);
+//   finish          r_v = the 2 x 3F partials + sum_f T_v[f][0] L_f[0].
+// No block barriers after the plane fills: every warp owns its vertex.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace hs {
+
+constexpr int kPN = 7;                    // log2 N of this path
+constexpr int kPG = 64;                   // level n-1 side
+constexpr int kPD1 = 4 * kPG * kPG;       // D1 floats
+constexpr int kPD2 = 16 * 32 * 32;        // D2 (and F2) floats
+constexpr int kPD3 = 2 * 64 * 16 * 16;    // level n-3 (detail, field) pairs, 64 residues
+constexpr int kPlanesPerUnit = kPD1 + 2 * kPD2 + kPD3;
+
+namespace {
+
+__device__ __forceinline__ float pw2(int e) { return __int_as_float((127 + e) << 23); }
+
+// one bottom-up cell (level LEV from the periodic plane src of side 2^(LEV+1) rolled by (ry, rx)):
+// the shifted field fv and the detail dv before its 2^-LEV scale (FLD: 0 = X -> H, 1 = Y -> V, 2 = Z -> D)
+template <typename V, int FLD>
+__device__ __forceinline__ void bu_rolled(const V* src, int Gs, int i, int j, int ry, int rx, V& fv, V& dv) {
+  const int m = Gs - 1;
+  const V* p0 = src + ((2 * i - ry) & m) * Gs;
+  const V* p1 = src + ((2 * i + 1 - ry) & m) * Gs;
+  const V* p2 = src + ((2 * i + 2 - ry) & m) * Gs;
+  const int c0 = (2 * j - rx) & m, c1 = (2 * j + 1 - rx) & m, c2 = (2 * j + 2 - rx) & m;
+  const V q = V(0.25);
+  if (FLD == 0) {
+    fv = q * (p0[c0] + V(2) * p0[c1] + p0[c2] + p1[c0] + V(2) * p1[c1] + p1[c2]);
+    dv = q * (p0[c0] + p1[c0]);
+  } else if (FLD == 1) {
+    fv = q * (p0[c0] + V(2) * p1[c0] + p2[c0] + p0[c1] + V(2) * p1[c1] + p2[c1]);
+    dv = q * (p0[c0] + p0[c1]);
+  } else {
+    fv = q * ((p0[c0] + V(2) * p0[c1] + p0[c2]) + V(2) * (p1[c0] + V(2) * p1[c1] + p1[c2]) +
+              (p2[c0] + V(2) * p2[c1] + p2[c2]));
+    dv = q * p0[c0];
+  }
+}
+
+// ------------------------------------------------------------------------------- precompute
+// fields64: the fp64 level-n fields [f][3][N][N] (natural layout) at stride face_stride doubles
+template <int FLD>
+__device__ void planes_body(const double* F, float* out, double* F1) {
+  // level n-1, residues rho in {0,1}^2:  P_{1,rho} = BU(roll(F, rho))
+  for (int idx = threadIdx.x; idx < 4 * kPG * kPG; idx += blockDim.x) {
+    const int rho = idx >> 12, cell = idx & 4095, i = cell >> 6, j = cell & 63;
+    double fv, dv;
+    bu_rolled<double, FLD>(F, 128, i, j, rho >> 1, rho & 1, fv, dv);
+    F1[idx] = fv;
+    out[idx] = (float)(dv * (double)pw2(-(kPN - 1)));
+  }
+  __syncthreads();
+  // level n-2, residues rho' in {0..3}^2:  P_{2,rho'} = BU(roll(P_{1, rho' mod 2}, rho' div 2))
+  float* D2 = out + kPD1;
+  float* F2 = D2 + kPD2;
+  for (int idx = threadIdx.x; idx < kPD2; idx += blockDim.x) {
+    const int rho = idx >> 10, cell = idx & 1023, i = cell >> 5, j = cell & 31;
+    const int ry = rho >> 2, rx = rho & 3;
+    double fv, dv;
+    bu_rolled<double, FLD>(F1 + (((ry & 1) << 1) | (rx & 1)) * 4096, 64, i, j, ry >> 1, rx >> 1, fv, dv);
+    D2[idx] = (float)(dv * (double)pw2(-(kPN - 2)));
+    F2[idx] = (float)fv;
+  }
+}
+
+__global__ void __launch_bounds__(512) planes_kernel(const double* __restrict__ fields64, long long face_stride,
+                                                     float* __restrict__ planes) {
+  extern __shared__ double F1s[];   // [4][64][64] fp64 level n-1 fields of the four residues
+  const int f = blockIdx.x / 3, t = blockIdx.x % 3;
+  const double* F = fields64 + (long long)f * face_stride + (long long)t * (1 << (2 * kPN));
+  float* out = planes + (long long)blockIdx.x * kPlanesPerUnit;
+  if (t == 0) planes_body<0>(F, out, F1s);
+  else if (t == 1) planes_body<1>(F, out, F1s);
+  else planes_body<2>(F, out, F1s);
+}
+
+// level n-3, residues rho'' in {0..7}^2:  P_{3,rho''} = BU(roll(P_{2, rho'' mod 4}, rho'' div 4)), from
+// the (fp32) level n-2 fields F2 of planes_kernel
+template <int FLD>
+__device__ void planes3_body(const float* F2, float2* DF3) {
+  for (int idx = threadIdx.x; idx < 64 * 256; idx += blockDim.x) {
+    const int rho = idx >> 8, cell = idx & 255, i = cell >> 4, j = cell & 15;
+    const int ry = rho >> 3, rx = rho & 7;
+    float fv, dv;
+    bu_rolled<float, FLD>(F2 + (((ry & 3) << 2) | (rx & 3)) * 1024, 32, i, j, ry >> 2, rx >> 2, fv, dv);
+    DF3[idx] = make_float2(dv * pw2(-(kPN - 3)), fv);
+  }
+}
+
+__global__ void __launch_bounds__(256) planes3_kernel(float* __restrict__ planes) {
+  const int t = blockIdx.x % 3;
+  float* base = planes + (long long)blockIdx.x * kPlanesPerUnit;
+  const float* F2 = base + kPD1 + kPD2;
+  float2* DF3 = reinterpret_cast<float2*>(base + kPD1 + 2 * kPD2);
+  if (t == 0) planes3_body<0>(F2, DF3);
+  else if (t == 1) planes3_body<1>(F2, DF3);
+  else planes3_body<2>(F2, DF3);
+}
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float lds(uint32_t a) {
+  float x;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a));   // planes are read-only after the fill
+  return x;
+}
+
+// ------------------------------------------------------------------------------- level n-1
+constexpr int kAWarps = 32;
+constexpr int kARows = 2 * kPG;   // D1 rows doubled: rows s .. s+63 never wrap
+constexpr int kASmem = (4 * kARows * kPG + kPD2) * 4;   // D1 doubled + D2
+
+__global__ void __launch_bounds__(kAWarps * 32, 1)
+    planes_a_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ planes,
+                    const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
+  extern __shared__ __align__(16) float D1s[];   // [4][128][64]
+  const int units = 3 * faces;
+  const int unit = blockIdx.x % units, split = blockIdx.x / units;
+  const int f = unit / 3, t = unit - 3 * (unit / 3);
+  const float* src = planes + (long long)unit * kPlanesPerUnit;
+  for (int idx = threadIdx.x; idx < 4 * kARows * kPG; idx += blockDim.x) {
+    const int rho = idx / (kARows * kPG), rem = idx - rho * (kARows * kPG);
+    const int r = rem >> 6, c = rem & 63;
+    D1s[idx] = __ldg(src + rho * 4096 + (r & 63) * 64 + c);
+  }
+  float* D2s = D1s + 4 * kARows * kPG;
+  for (int idx = threadIdx.x; idx < kPD2; idx += blockDim.x) D2s[idx] = __ldg(src + kPD1 + idx);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long NN = 1ll << (2 * kPN);
+  const long long Kt = (long long)faces * NN;
+  const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
+  const uint32_t base = saddr(D1s);
+  for (long long v = v0 + warp; v < v1; v += kAWarps) {
+    const int4 pr = __ldg(vparams + v);
+    const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w);
+    const float* Tl = T + v * Kt + (long long)f * NN + (long long)(1 + t) * 4096 + lane;
+    // combo (a, b): Q = q + (a, b) mod N; residue Q & 1, roll Q >> 1
+    uint32_t ad[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int Qy = (pr.x + a) & 127;
+      const int s = (-(Qy >> 1)) & 63;   // D1 row of output row 0
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int Qx = (pr.y + b) & 127;
+        const int rho = ((Qy & 1) << 1) | (Qx & 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          ad[a][b][c] = base + (uint32_t)(((rho * kARows + s) * 64 + ((lane + 32 * c - (Qx >> 1)) & 63)) * 4);
+      }
+    }
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll 8
+    for (int i = 0; i < kPG; ++i) {
+      const float t0 = __ldg(Tl + i * 64), t1 = __ldg(Tl + i * 64 + 32);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          acc[a][b] = fmaf(t0, lds(ad[a][b][0] + i * 256), acc[a][b]);
+          acc[a][b] = fmaf(t1, lds(ad[a][b][1] + i * 256), acc[a][b]);
+        }
+    }
+    // level n-2 details: residue Q & 3, roll Q >> 2; lanes = columns (conflict-free), rows wrapped
+    const float* T2 = T + v * Kt + (long long)f * NN + (long long)(1 + t) * 1024 + lane;
+    int off2[2][2], ry2[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      ry2[a] = ((pr.x + a) & 127) >> 2;
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+        off2[a][b] = ((((pr.x + a) & 3) << 2) | ((pr.y + b) & 3)) * 1024 + ((lane - (((pr.y + b) & 127) >> 2)) & 31);
+    }
+    float acc2[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const float t2 = __ldg(T2 + i * 32);
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int row = ((i - ry2[a]) & 31) * 32;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) acc2[a][b] = fmaf(t2, D2s[off2[a][b] + row], acc2[a][b]);
+      }
+    }
+    const float wy0 = 1.f - wy1, wx0 = 1.f - wx1;
+    float r = wy0 * (wx0 * (acc[0][0] + acc2[0][0]) + wx1 * (acc[0][1] + acc2[0][1])) +
+              wy1 * (wx0 * (acc[1][0] + acc2[1][0]) + wx1 * (acc[1][1] + acc2[1][1]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) partial[v * 2 * units + unit] = r;
+  }
+}
+
+// ------------------------------------------------------------------------------- level n-3 .. 0
+constexpr int kCWarps = 32;
+constexpr int kCScr = 256 + 64 + 16 + 4;   // per warp: level n-3, 3, 2, 1 planes
+constexpr int kCSmem = (kPD3 + kCWarps * kCScr) * 4;
+
+template <int FLD>
+__device__ __forceinline__ float planes_c_vertex(const float2* DF3s, float* S3, const float* __restrict__ Tv, int4 pr,
+                                                 int lane) {
+  // T values of levels n-3 .. 0 of this type, requested first
+  float t3[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t3[k] = __ldg(Tv + (1 + FLD) * 256 + lane + 32 * k);
+  const float t4a = __ldg(Tv + (1 + FLD) * 64 + lane), t4b = __ldg(Tv + (1 + FLD) * 64 + 32 + lane);
+  const float t5 = lane < 16 ? __ldg(Tv + (1 + FLD) * 16 + lane) : 0.f;
+  const float t6 = lane < 4 ? __ldg(Tv + (1 + FLD) * 4 + lane) : 0.f;
+  const float t7 = lane < 1 ? __ldg(Tv + (1 + FLD)) : 0.f;
+  const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
+  const float w[2][2] = {{wy0 * wx0, wy0 * wx1}, {wy1 * wx0, wy1 * wx1}};
+  // combo (a, b): Q = q + (a, b); residue Q & 7, roll Q >> 3.  Cell lane + 32 k = (row 2k + lane / 16,
+  // column lane % 16): a half-warp reads one rolled 16-wide row
+  const int jl = lane & 15, il = lane >> 4;
+  int off[2][2], ry[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    ry[a] = ((pr.x + a) & 127) >> 3;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+      off[a][b] = ((((pr.x + a) & 7) << 3) | ((pr.y + b) & 7)) * 256 + ((jl - (((pr.y + b) & 127) >> 3)) & 15);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = 2 * k + il;
+    float d = 0.f, fv = 0.f;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int row = ((i - ry[a]) & 15) * 16;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const float2 p = DF3s[off[a][b] + row];
+        d = fmaf(w[a][b], p.x, d);
+        fv = fmaf(w[a][b], p.y, fv);
+      }
+    }
+    S3[lane + 32 * k] = fv;
+    acc = fmaf(d, t3[k], acc);
+  }
+  __syncwarp();
+  float* W3 = S3 + 256;
+  float* W2 = W3 + 64;
+  float* W1 = W2 + 16;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = lane + 32 * k;
+    float f2, dv;
+    bu_rolled<float, FLD>(S3, 16, idx >> 3, idx & 7, 0, 0, f2, dv);
+    W3[idx] = f2;
+    acc = fmaf(dv * pw2(-3), k ? t4b : t4a, acc);
+  }
+  __syncwarp();
+  if (lane < 16) {
+    float f2, dv;
+    bu_rolled<float, FLD>(W3, 8, lane >> 2, lane & 3, 0, 0, f2, dv);
+    W2[lane] = f2;
+    acc = fmaf(dv * pw2(-2), t5, acc);
+  }
+  __syncwarp();
+  if (lane < 4) {
+    float f2, dv;
+    bu_rolled<float, FLD>(W2, 4, lane >> 1, lane & 1, 0, 0, f2, dv);
+    W1[lane] = f2;
+    acc = fmaf(dv * pw2(-1), t6, acc);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    float f2, dv;
+    bu_rolled<float, FLD>(W1, 2, 0, 0, 0, 0, f2, dv);
+    acc = fmaf(dv, t7, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __syncwarp();   // S3 .. W1 are rewritten by this warp's next vertex
+  return acc;
+}
+
+__global__ void __launch_bounds__(kCWarps * 32, 1)
+    planes_c_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ planes,
+                    const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
+  extern __shared__ __align__(16) float smC[];
+  const float2* DF3s = reinterpret_cast<const float2*>(smC);
+  const int units = 3 * faces;
+  const int unit = blockIdx.x % units, split = blockIdx.x / units;
+  const int f = unit / 3, t = unit - 3 * (unit / 3);
+  const float* src = planes + (long long)unit * kPlanesPerUnit + kPD1 + 2 * kPD2;
+  for (int idx = threadIdx.x; idx < kPD3; idx += blockDim.x) smC[idx] = __ldg(src + idx);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* S3 = smC + kPD3 + warp * kCScr;
+  const long long NN = 1ll << (2 * kPN);
+  const long long Kt = (long long)faces * NN;
+  const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
+  for (long long v = v0 + warp; v < v1; v += kCWarps) {
+    const int4 pr = __ldg(vparams + v);
+    const float* Tv = T + v * Kt + (long long)f * NN;
+    float r;
+    if (t == 0) r = planes_c_vertex<0>(DF3s, S3, Tv, pr, lane);
+    else if (t == 1) r = planes_c_vertex<1>(DF3s, S3, Tv, pr, lane);
+    else r = planes_c_vertex<2>(DF3s, S3, Tv, pr, lane);
+    if (lane == 0) partial[v * 2 * units + units + unit] = r;
+  }
+}
+
+__global__ void planes_finish_kernel(const float* __restrict__ partial, const float* __restrict__ T,
+                                     const float* __restrict__ light, long long V, int faces, float* __restrict__ R) {
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int units = 3 * faces;
+  const long long NN = 1ll << (2 * kPN);
+  float s = 0.f;
+  for (int u = 0; u < 2 * units; ++u) s += partial[v * 2 * units + u];
+  for (int f = 0; f < faces; ++f) s = fmaf(__ldg(T + v * faces * NN + f * NN), __ldg(light + f * NN), s);
+  R[v] = s;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+size_t relight_planes_workspace_bytes(long long V, int faces) {
+  return (size_t)faces * 3 * kPlanesPerUnit * 4 + (size_t)V * 6 * faces * 4 + 256;
+}
+
+// fields64: fp64 level-n fields of face f at fields64 + f * face_stride, [3][N][N]
+hs_status launch_relight_planes(const float* T, long long V, int faces, const float* light, const double* fields64,
+                                long long face_stride, const int4* vparams, float* R, void* ws, cudaStream_t st) {
+  float* planes = reinterpret_cast<float*>(ws);
+  float* partial = planes + (size_t)faces * 3 * kPlanesPerUnit;
+  const int units = 3 * faces;
+  static bool attr = false;
+  if (!attr) {
+    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4096 * 8),
+                  "cudaFuncSetAttribute(planes_kernel)");
+    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem),
+                  "cudaFuncSetAttribute(planes_a_kernel)");
+    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem),
+                  "cudaFuncSetAttribute(planes_c_kernel)");
+    attr = true;
+  }
+  planes_kernel<<<units, 512, 4 * 4096 * 8, st>>>(fields64, face_stride, planes);
+  HS_CHECK_LAUNCH("planes_kernel");
+  planes3_kernel<<<units, 256, 0, st>>>(planes);
+  HS_CHECK_LAUNCH("planes3_kernel");
+  int nsplit = sm_count() / units;
+  if (nsplit < 1) nsplit = 1;
+  if (nsplit > V) nsplit = (int)V;
+  planes_a_kernel<<<units * nsplit, kAWarps * 32, kASmem, st>>>(T, V, faces, planes, vparams, partial, nsplit);
+  HS_CHECK_LAUNCH("planes_a_kernel");
+  planes_c_kernel<<<units * nsplit, kCWarps * 32, kCSmem, st>>>(T, V, faces, planes, vparams, partial, nsplit);
+  HS_CHECK_LAUNCH("planes_c_kernel");
+  planes_finish_kernel<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(partial, T, light, V, faces, R);
+  HS_CHECK_LAUNCH("planes_finish_kernel");
+  return HS_OK;
+}
+
+}  // namespace hs

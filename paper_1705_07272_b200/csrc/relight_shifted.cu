@@ -89,12 +89,13 @@ __global__ void __launch_bounds__(kThreads) fields_kernel(const float* __restric
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int r = 2 * i + a, c = 2 * j + b;
-          if (!last) {
+          {   // natural layout, fp64 (the last level is read by the N = 128 residue planes)
             const int o = r * G + c;
             nxt[o] = cx[a][b];
             nxt[G * G + o] = cy[a][b];
             nxt[2 * G * G + o] = cz[a][b];
-          } else {
+          }
+          if (last) {
             // final layout: [f][t][parity][r][c/2]
             float* base = fields + (long long)f * 3 * NN;
             const long long o = (long long)(c & 1) * (NN / 2) + (long long)r * (N / 2) + (c >> 1);
@@ -741,7 +742,8 @@ bool relight_shifted_fused_supported(int log2n) { return log2n >= 5 && log2n <= 
 size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n) {
   const size_t NN = (size_t)1 << (2 * log2n);
   return (size_t)faces * 3 * NN * 4 /*fields*/ + (size_t)faces * 6 * NN * 8 /*fp64 scratch*/ +
-         (size_t)V * 3 * faces * 4 /*partials*/ + (size_t)V * 16 /*vertex params*/ + 512;
+         (size_t)V * 3 * faces * 4 /*partials*/ + (size_t)V * 16 /*vertex params*/ + 512 +
+         (log2n == 7 ? relight_planes_workspace_bytes(V, faces) + 256 : 0);
 }
 
 hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, const float* light, int log2n,
@@ -755,11 +757,14 @@ hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, c
   HS_CHECK_LAUNCH("fields_kernel");
   vertex_params_kernel<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(shifts, V, 1 << log2n, vp);
   HS_CHECK_LAUNCH("vertex_params_kernel");
+  if (log2n == 7) {   // residue planes (csrc/relight_planes.cu)
+    void* pws = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(vp + V) + 255) & ~uintptr_t(255));
+    return launch_relight_planes(T, V, faces, light, scratch + 3 * NN, (long long)(6 * NN), vp, R, pws, st);
+  }
   hs_status s = HS_OK;
   switch (log2n) {
     case 5: s = launch_unit<5>(T, V, faces, fields, vp, partial, st); break;
     case 6: s = launch_unit<6>(T, V, faces, fields, vp, partial, st); break;
-    case 7: s = launch_unit<7>(T, V, faces, fields, vp, partial, st); break;
     default: return HS_ERR_UNSUPPORTED;
   }
   if (s != HS_OK) return s;
