@@ -16,6 +16,8 @@
 //   finish  : r_v = sum over units of the partials + sum_f T_v[f][0] L_f[0] (the scaling
 //             coefficient is shift invariant).
 // Every shift is processed at the finest level (integer shifts have phi = 0), which is exact.
+// N = 32, 64 run the unit kernels below; N = 128 precomputes residue planes of the light and
+// reads them per vertex instead (csrc/relight_planes.cu), fed by fields_kernel's fp64 fields.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -111,26 +113,6 @@ __global__ void __launch_bounds__(kThreads) fields_kernel(const float* __restric
 }
 
 // ------------------------------------------------------------------------------- main
-// Packed fp32 pairs (sm_100 FFMA2): the two level n-1 columns a thread owns share every weight, so
-// their filters issue as one f32x2 instruction (half the FMA-pipe instructions of scalar code).
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {   // a * b + c
-  float2 r;
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(r.x), "=f"(r.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return r;
-}
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
-  float2 r;
-  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(r.x), "=f"(r.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
-__device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
-
 constexpr int qpp_pad(int qp, int rows) {   // smallest row length >= qp with rows * q = 16 (mod 32)
   int q = qp;
   while ((rows * q) % 32 != 16) ++q;
@@ -141,8 +123,8 @@ template <int LOG2N>
 struct Geo {
   static constexpr int N = 1 << LOG2N;
   static constexpr int G = N / 2;                  // level n-1 side
-  // adjacent level n-1 columns per thread: 2 at N = 128 (6 taps for 2 outputs, filters in f32x2)
-  static constexpr int CPT = LOG2N >= 7 ? 2 : 1;
+  // level n-1 columns per thread (N = 128 takes the residue-plane path, csrc/relight_planes.cu)
+  static constexpr int CPT = 1;
   static constexpr int TPR = G / CPT;              // threads per level n-1 row
   static constexpr int NS = kThreads / TPR;        // row strips at level n-1
   static constexpr int RS = G / NS;                // output rows per strip
@@ -154,12 +136,7 @@ struct Geo {
   static constexpr int QP = N / SPLIT;
   static constexpr int QPP = TPR >= 32 ? QP : qpp_pad(QP, 2 * RS);
   static constexpr int PLANE = (N + PADR) * QPP;   // one column-class plane, padded
-  // one vertex group's scratch.  CPT 1: S1, S2, red, T block (level n-1).  CPT 2: two T buffers
-  // (level n-1 and n-2 blocks), two S2, S3, warp-level planes, red -- level n-1 never goes
-  // through shared memory.
-  static constexpr int TBUF = G * G + (G / 2) * (G / 2);
-  static constexpr int SCR = CPT == 2 ? 2 * TBUF + 2 * (G / 2) * (G / 2) + (G / 4) * (G / 4) + 84 + 16 + 4
-                                      : 2 * G * G + (G / 2) * (G / 2) + 64;
+  static constexpr int SCR = 2 * G * G + (G / 2) * (G / 2) + 64;   // one vertex group: S1, S2, red, T block
   static constexpr int smem(int vg) { return (SPLIT * PLANE + vg * SCR) * 4; }
   static_assert(kThreads % TPR == 0 && G % NS == 0 && TPR >= 16, "geometry");
 };
@@ -177,32 +154,6 @@ __global__ void vertex_params_kernel(const float* __restrict__ shifts, long long
 
 // Named barrier of one vertex group (256 threads; ids 1.. -- id 0 is __syncthreads).
 __device__ __forceinline__ void group_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kThreads) : "memory"); }
-// Producer side of the same barrier: count this warp in without waiting.
-__device__ __forceinline__ void group_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kThreads) : "memory"); }
-
-// One bottom-up cell of level LEV from the periodic level LEV+1 plane src (side 2^(LEV+1)):
-// fv = the shifted field at level LEV, dv = the detail before its 2^-LEV scale (as bottom_up)
-template <int FLD, int LEV>
-__device__ __forceinline__ void bu_cell(const float* src, int idx, float& fv, float& dv) {
-  constexpr int g = 1 << LEV, Gs = 2 * g;
-  const int i = idx >> LEV, jj = idx & (g - 1);
-  const float* p0 = src + (2 * i) * Gs;
-  const float* p1 = p0 + Gs;
-  const float* p2 = src + ((2 * i + 2) & (Gs - 1)) * Gs;
-  const int c0 = 2 * jj, c1 = 2 * jj + 1, c2 = (2 * jj + 2) & (Gs - 1);
-  if (FLD == 0) {
-    fv = 0.25f * (p0[c0] + 2.f * p0[c1] + p0[c2] + p1[c0] + 2.f * p1[c1] + p1[c2]);
-    dv = 0.25f * (p0[c0] + p1[c0]);
-  } else if (FLD == 1) {
-    fv = 0.25f * (p0[c0] + 2.f * p1[c0] + p2[c0] + p0[c1] + 2.f * p1[c1] + p2[c1]);
-    dv = 0.25f * (p0[c0] + p0[c1]);
-  } else {
-    fv = 0.25f * ((p0[c0] + 2.f * p0[c1] + p0[c2]) + 2.f * (p1[c0] + 2.f * p1[c1] + p1[c2]) +
-                  (p2[c0] + 2.f * p2[c1] + p2[c2]));
-    dv = 0.25f * p0[c0];
-  }
-}
-
 // One bottom-up level LEV (and, recursively, all coarser ones): shifted fields of level LEV from
 // level LEV+1 (periodic), the detail output dotted with T_v's coefficients of type FLD.  Levels
 // with more than 64 cells use the whole vertex group (named barrier between levels); the last
@@ -424,219 +375,6 @@ __device__ __forceinline__ void unit_body1(const float* plane, float* scratch, u
   }
 }
 
-// CPT = 2 (N = 128): a warp owns whole level n-1 rows (G = 64 = 2 x 32 columns), so level n-1
-// stays in registers and level n-2 is computed inside the stencil (column 2t+2 by a shuffle from
-// lane t+1, periodic within the warp); the shared-memory bottom-up starts at level n-3.  The
-// columns j, j+1 of a thread are f32x2 pairs (tap pairs (x[k], x[k+2])).  T_v's level n-1 and n-2
-// blocks of type FLD (contiguous) are bulk-copied one vertex ahead into a double buffer.
-template <int LOG2N, int FLD, int VG>
-__device__ __forceinline__ void unit_body2(const float* plane, float* scratch, uint64_t* mbars, const float* __restrict__ T,
-                                           int faces, int f, const int4* __restrict__ vparams, float* __restrict__ partial,
-                                           int unit, int units, long long v0, long long v1) {
-  using Gm = Geo<LOG2N>;
-  constexpr int N = Gm::N, G = Gm::G, RS = Gm::RS, QPP = Gm::QPP, PLANE = Gm::PLANE, SPLIT = Gm::SPLIT;
-  constexpr int n = LOG2N;
-  static_assert(Gm::CPT == 2 && G == 64 && Gm::TPR == 32, "a warp holds one level n-1 row");
-  static_assert(1 + 2 * VG <= 16, "named barriers");
-  constexpr int NTK = (FLD == 1) ? 5 : 6;
-  const int grp = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
-  const int bar = 1 + grp;
-  float* Tbuf = scratch + grp * Gm::SCR;          // [2][G*G + G*G/4]
-  // level n-2 (G/2 x G/2), double-buffered by vertex parity: warps that finish level n-3 run
-  // ahead into the next vertex's stencil while others may still read this one
-  float* S2b = Tbuf + 2 * Gm::TBUF;
-  float* S3 = S2b + 2 * (G / 2) * (G / 2);        // level n-3
-  float* W = S3 + (G / 4) * (G / 4);              // warp levels 3, 2, 1 (64 + 16 + 4)
-  float* red = W + 84;                            // [2][8] per-warp partial sums (vertex parity)
-  uint64_t* mb = mbars + 2 * grp;
-  const long long NN = (long long)N * N;
-  const long long Kt = (long long)faces * NN;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int j = 2 * lane;                         // level n-1 columns j, j+1
-  const int i0 = warp * RS;                       // first level n-1 row of this warp's strip
-  constexpr uint32_t TB_BYTES = Gm::TBUF * 4;
-  // T_v's type-FLD blocks: level n-2 at (1+FLD) 4^(n-2), level n-1 at (1+FLD) 4^(n-1) -- copied
-  // as [level n-1 block][level n-2 block]
-  auto issue = [&](long long vv, int b) {
-    const float* Tv = T + vv * Kt + (long long)f * NN;
-    float* dst = Tbuf + b * Gm::TBUF;
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mb + b)),
-                 "r"(TB_BYTES) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)), "l"(Tv + ((long long)(1 + FLD) << (2 * (n - 1)))), "r"(G * G * 4),
-                 "r"(smem_addr(mb + b)) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst + G * G)), "l"(Tv + ((long long)(1 + FLD) << (2 * (n - 2)))), "r"(G * G), 
-                 "r"(smem_addr(mb + b)) : "memory");
-  };
-  if (tid == 0 && v0 + grp < v1) issue(v0 + grp, 0);
-  uint32_t phases = 0;   // bit b: parity of buffer b
-  int b = 0;
-  int4 pr_next = (v0 + grp < v1) ? __ldg(vparams + v0 + grp) : make_int4(0, 0, 0, 0);
-  int it = 0;   // vertex iteration of this group
-  for (long long v = v0 + grp; v < v1; v += VG, b ^= 1, ++it) {
-    const int4 pr = pr_next;   // loaded one vertex ahead (its latency was on the critical path)
-    if (v + VG < v1) pr_next = __ldg(vparams + v + VG);
-    const float* Tv = T + v * Kt + (long long)f * NN;
-    const int qy = pr.x, qx = pr.y;
-    const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
-    // coarse-level T values, in flight during the stencil: level n-3 (one cell per thread) and,
-    // for the warp that runs levels 3 .. 0 of this vertex (rotating, so no warp lags), those
-    static_assert(LOG2N - 3 == 4, "level n-3 is the last group-wide level");
-    const int wl = it & 7;
-    const float t3 = __ldg(Tv + ((long long)(1 + FLD) << (2 * (n - 3))) + tid);
-    float tw[5];
-    if (warp == wl) {
-      tw[0] = __ldg(Tv + (1 + FLD) * 64 + lane);
-      tw[1] = __ldg(Tv + (1 + FLD) * 64 + lane + 32);
-      tw[2] = lane < 16 ? __ldg(Tv + (1 + FLD) * 16 + lane) : 0.f;
-      tw[3] = lane < 4 ? __ldg(Tv + (1 + FLD) * 4 + lane) : 0.f;
-      tw[4] = lane < 1 ? __ldg(Tv + (1 + FLD)) : 0.f;
-    }
-    const int rs = (2 * i0 - qy - 1) & (N - 1);
-    uint32_t base[NTK];   // shared addresses of the taps at window row 0 (c = 2j - qx - 1 + k)
-#pragma unroll
-    for (int k = 0; k < NTK; ++k) {
-      const int c = (2 * j - qx + k - 1) & (N - 1);
-      base[k] = smem_addr(plane + (c % SPLIT) * PLANE + rs * QPP + c / SPLIT);
-    }
-    // weights with the level scales folded in (powers of two: exact).  X, Z: horizontal tent x 1/4
-    // (hA feeds only the field), detail taps x 2^-(n-1)/4 (hB feeds only the detail); Y shares hA
-    // and hB, so its scales go on the vertical weights
-    const float qd = 0.25f * pow2f(-(n - 1));
-    const float sh = (FLD == 1) ? 1.f : 0.25f, sd = (FLD == 1) ? 1.f : qd;
-    const float2 TA = dup2(sh * wx1), TB0 = dup2(sh * (wx0 + 2.f * wx1)), TB1 = dup2(sh * (2.f * wx0 + wx1)),
-                 TC = dup2(sh * wx0), DX1 = dup2(sd * wx1), DX0 = dup2(sd * wx0);
-    const float vf = (FLD == 1) ? 0.25f : 1.f, vd = (FLD == 1) ? qd : 1.f;
-    const float2 UA = dup2(vf * wy1), UB0 = dup2(vf * (wy0 + 2.f * wy1)), UB1 = dup2(vf * (2.f * wy0 + wy1)),
-                 UC = dup2(vf * wy0), FY1 = dup2(vf * wy1), FY0 = dup2(vf * wy0), DY1 = dup2(vd * wy1),
-                 DY0 = dup2(vd * wy0);
-    mbar_wait_parity(mb + b, (phases >> b) & 1);   // T_v's blocks have landed
-    phases ^= 1u << b;
-    if (tid == 0 && v + VG < v1) issue(v + VG, b ^ 1);   // the other buffer was released last vertex
-    float* S2 = S2b + b * (G / 2) * (G / 2);
-    const float* Tb1 = Tbuf + b * Gm::TBUF;          // level n-1 block
-    const float* Tb2 = Tb1 + G * G;                  // level n-2 block
-    constexpr int LAST = (FLD == 0) ? 2 : 3;
-    constexpr int ROWS = RS + (FLD == 0 ? 0 : 1);    // Y, Z also need the next strip's first row
-    constexpr int NU = LAST + 2 * (ROWS - 1) + 1;    // window rows read
-    const float qo2 = 0.25f * pow2f(-(n - 2));
-    float2 hA[NU], hB[NU];
-    float ra[ROWS], rb[ROWS], rc[ROWS];              // level n-1 columns 2t, 2t+1, 2t+2
-    float2 acc2 = make_float2(0.f, 0.f);
-    float acc1 = 0.f;
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-      float x[NTK];
-#pragma unroll
-      for (int k = 0; k < NTK; ++k) x[k] = lds(base[k] + u * QPP * 4);
-      const float2 p0 = make_float2(x[0], x[2]), p1 = make_float2(x[1], x[3]), p2 = make_float2(x[2], x[4]);
-      if (FLD == 1) {
-        hA[u] = ffma2(DX1, p0, ffma2(DX0, p2, p1));      // shifted [1, 1] with the unit tap in the middle
-        hB[u] = hA[u];
-      } else {
-        const float2 p3 = make_float2(x[3], x[5 < NTK ? 5 : 0]);
-        hA[u] = ffma2(TA, p0, ffma2(TB0, p1, ffma2(TB1, p2, fmul2(TC, p3))));
-        hB[u] = ffma2(DX1, p0, fmul2(DX0, p1));
-      }
-      if (u >= LAST && ((u - LAST) & 1) == 0) {
-        const int r = (u - LAST) >> 1;
-        const int w = 2 * r;
-        float2 fl;
-        if (FLD == 0) fl = ffma2(FY1, hA[w], ffma2(FY0, hA[w + 2], hA[w + 1]));   // X: vf = 1
-        else fl = ffma2(UA, hA[w], ffma2(UB0, hA[w + 1], ffma2(UB1, hA[w + 2], fmul2(UC, hA[w + 3]))));
-        if (r < RS) {
-          float2 det;
-          if (FLD == 0) det = ffma2(DY1, hB[w], ffma2(DY0, hB[w + 2], hB[w + 1]));
-          else det = ffma2(DY1, hB[w], fmul2(DY0, hB[w + 1]));
-          acc2 = ffma2(det, *reinterpret_cast<const float2*>(Tb1 + (i0 + r) * G + j), acc2);
-        }
-        ra[r] = fl.x;
-        rb[r] = fl.y;
-        rc[r] = __shfl_sync(0xffffffffu, fl.x, (lane + 1) & 31);
-        // level n-2 cell (i0/2 + c2, lane) once its rows are in: X needs rows 2c2, 2c2+1; Y, Z 2c2 .. 2c2+2
-        constexpr int NEED = (FLD == 0) ? 1 : 2;
-        if (r >= NEED && ((r - NEED) & 1) == 0) {
-          const int c2 = (r - NEED) >> 1;
-          const int a = 2 * c2;
-          float fv, dv;
-          if (FLD == 0) {
-            fv = 0.25f * (ra[a] + 2.f * rb[a] + rc[a] + ra[a + 1] + 2.f * rb[a + 1] + rc[a + 1]);
-            dv = ra[a] + ra[a + 1];
-          } else if (FLD == 1) {
-            fv = 0.25f * (ra[a] + 2.f * ra[a + 1] + ra[a + 2] + rb[a] + 2.f * rb[a + 1] + rb[a + 2]);
-            dv = ra[a] + rb[a];
-          } else {
-            fv = 0.25f * ((ra[a] + 2.f * rb[a] + rc[a]) + 2.f * (ra[a + 1] + 2.f * rb[a + 1] + rc[a + 1]) +
-                          (ra[a + 2] + 2.f * rb[a + 2] + rc[a + 2]));
-            dv = ra[a];
-          }
-          const int o2 = (i0 / 2 + c2) * (G / 2) + lane;
-          S2[o2] = fv;
-          acc1 = fmaf(dv * qo2, Tb2[o2], acc1);
-        }
-      }
-    }
-    float acc = acc1 + (acc2.x + acc2.y);
-    group_sync(bar);   // S2 complete; this vertex's T buffer is released
-    {                  // level n-3: 256 cells, one per thread
-      float fv, dv;
-      bu_cell<FLD, LOG2N - 3>(S2, tid, fv, dv);
-      S3[tid] = fv;
-      acc = fmaf(dv * pow2f(-(n - 3)), t3, acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    float* rd = red + 8 * b;
-    if (lane == 0) rd[warp] = acc;
-    // a barrier of its own (ids 1 + VG ..): a warp that arrives here and runs ahead reaches the
-    // group barrier of the next vertex before this one has necessarily completed
-    const int bar2 = 1 + VG + grp;
-    if (warp != wl) {
-      group_arrive(bar2);   // S3 and this warp's partial are published; go on to the next vertex
-      continue;
-    }
-    group_sync(bar2);
-    // levels 3 .. 0 on warp wl (warp-synchronous), then the fixed-order sum of the partials
-    float aw = 0.f;
-    {
-      float fv, dv;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        bu_cell<FLD, 3>(S3, lane + 32 * k, fv, dv);
-        W[lane + 32 * k] = fv;
-        aw = fmaf(dv * pow2f(-3), tw[k], aw);
-      }
-      __syncwarp();
-      if (lane < 16) {
-        bu_cell<FLD, 2>(W, lane, fv, dv);
-        W[64 + lane] = fv;
-        aw = fmaf(dv * pow2f(-2), tw[2], aw);
-      }
-      __syncwarp();
-      if (lane < 4) {
-        bu_cell<FLD, 1>(W + 64, lane, fv, dv);
-        W[80 + lane] = fv;
-        aw = fmaf(dv * pow2f(-1), tw[3], aw);
-      }
-      __syncwarp();
-      if (lane < 1) {
-        bu_cell<FLD, 0>(W + 80, lane, fv, dv);
-        aw = fmaf(dv, tw[4], aw);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
-    if (lane == 0) {
-      float sum = 0.f;
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) sum += rd[w];
-      partial[v * units + unit] = sum + aw;
-    }
-    __syncwarp();
-  }
-}
-
 template <int LOG2N, int VG>
 __global__ void __launch_bounds__(kThreads * VG, 1)
     relight_shifted_unit_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ fields,
@@ -662,21 +400,15 @@ __global__ void __launch_bounds__(kThreads * VG, 1)
       }
     }
   }
-  __shared__ __align__(8) uint64_t mbars[2 * VG];
-  if (threadIdx.x < 2 * VG) mbar_init1(&mbars[threadIdx.x]);
+  __shared__ __align__(8) uint64_t mbars[VG];
+  if (threadIdx.x < VG) mbar_init1(&mbars[threadIdx.x]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
   float* scratch = sm + SPLIT * PLANE;
-  if constexpr (Gm::CPT == 2) {
-    if (t == 0) unit_body2<LOG2N, 0, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-    else if (t == 1) unit_body2<LOG2N, 1, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-    else unit_body2<LOG2N, 2, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-  } else {
-    if (t == 0) unit_body1<LOG2N, 0, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-    else if (t == 1) unit_body1<LOG2N, 1, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-    else unit_body1<LOG2N, 2, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
-  }
+  if (t == 0) unit_body1<LOG2N, 0, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else if (t == 1) unit_body1<LOG2N, 1, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
+  else unit_body1<LOG2N, 2, VG>(sm, scratch, mbars, T, faces, f, vparams, partial, unit, units, v0, v1);
 }
 
 __global__ void relight_shifted_finish_kernel(const float* __restrict__ partial, const float* __restrict__ T,

@@ -209,3 +209,23 @@ def test_shift_coarse_fuzz(case):
             ref = oshift.shift_coeffs_coarse2d(c[b, f], L0, *sh[b, f])[:4 ** band]
             err = np.linalg.norm(got[b, f] - ref) / max(np.linalg.norm(ref), 1e-30)
             assert err <= 1e-5, (n, L0, band, b, f, err)
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_relight_shifted_fuzz_n128(case):
+    """N = 128 (the residue-plane path): random face counts, ragged vertex counts, every shift class
+    including exact integers, halves and negatives"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    rng = np.random.default_rng(5500 + case)
+    n, N = 7, 128
+    faces = int(rng.integers(1, 7))
+    V = int(rng.integers(1, 40))
+    L = synth.light_pyramids(case, 1, faces, n)[0]
+    T = synth.transfer_rows(case, int(rng.integers(0, 10 ** 6)), V, faces, N * N)
+    vs = np.array([[_shift_value(rng, N), _shift_value(rng, N)] for _ in range(V)], dtype=np.float32)
+    got = hs.relight_vertices_shifted(torch.from_numpy(T).cuda(), torch.from_numpy(L).cuda(),
+                                      torch.from_numpy(vs).cuda()).cpu().numpy()
+    ref = orelight.relight_shifted(T, L, vs.astype(np.float64))
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 1e-5, (faces, V, err)
