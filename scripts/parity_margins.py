@@ -68,6 +68,28 @@ rq = hs.haar_pack_qtree(t(rho).view(2000, F, 1024), 5)
 vq = hs.haar_pack_qtree(t(vis).view(2000, F, 1024), 5)
 R = hs.relight_vertices_triple(rq, vq, full, F, 1024).cpu().numpy()
 out["c5t radiance (2000 vertices)"] = rel(R, orelight.relight_triple(rho, vis, ref_full[:, :, :1024], F, 1024))
+# c4: the full 100k-vertex job on the fused path (residue planes at N = 128), 24 sampled vertices
+cfg4 = synth.config("c4")
+V4, F4, n4 = cfg4.vertices, cfg4.faces, cfg4.log2n
+T4 = torch.empty((V4, F4 * 4 ** n4), dtype=torch.float32, device="cuda")
+hs.hs_fill_transfer(T4, 0, F4, 4 ** n4, cfg4.seed, synth.STREAM_T)
+L4 = synth.light_pyramids(cfg4.seed, 1, F4, n4)[0]
+sv4 = synth.c4_vertex_shifts(cfg4.seed, V4, n4)
+R4 = hs.relight_vertices_shifted(T4, t(L4), t(sv4)).cpu().numpy()
+del T4
+rows4 = np.unique(np.concatenate([[0, V4 - 1], rng.integers(0, V4, 22)]))
+ref4 = np.array([orelight.relight_shifted(synth.transfer_rows(cfg4.seed, int(v), 1, F4, 4 ** n4), L4,
+                                          sv4[v:v + 1].astype(np.float64))[0] for v in rows4])
+out[f"c4 radiance ({len(rows4)} sampled vertices)"] = rel(R4[rows4], ref4)
+# c6r: rotation of 4096 maps of 64^2 against the chain-rule oracle, 16 sampled maps
+from oracle import rotate as orot  # noqa: E402
+cfg6 = synth.config("c6r")
+maps6 = synth.smooth_sphere_maps(cfg6.seed, cfg6.frames, cfg6.log2n)
+ang6 = synth.rotation_angles(cfg6.seed, cfg6.frames)
+got6 = hs.haar_rotate_coeffs(t(maps6), ang6).cpu().numpy()
+pick = rng.integers(0, cfg6.frames, 16)
+out["c6r rotated maps (16 sampled, max)"] = max(rel(got6[b], orot.rotate_coeffs_chain(maps6[b], *ang6[b]))
+                                                for b in pick)
 torch.cuda.synchronize()
 for k, v in out.items():
     print(f"{k:42s} {v:.3e}  ({'ok' if v <= 1e-5 else 'OVER'}; margin x{1e-5 / v:.1f})")
