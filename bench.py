@@ -757,6 +757,44 @@ def run_sparse(args, cfg):
                      "note": "bound by L2 gathers (K_s x 64 frames x 4 B per vertex), not HBM"},
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": None,
     }
+    if not args.no_e2e:
+        # end to end: pinned host light in, pinned host radiance out, every step
+        light_h = torch.from_numpy(light_np).pin_memory()
+        Rh = torch.empty(R.shape, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            light.copy_(light_h, non_blocking=True)
+            step()
+            Rh.copy_(R, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.steps
+        line["e2e"] = {"value": V / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(light_np.nbytes),
+                       "d2h_bytes_per_step": int(R.numel() * 4)}
+    if not args.no_cpu_baseline:
+        from oracle import relight as orelight
+        from oracle import shift as oshift
+        rows = 400000   # a few seconds of oracle work
+        t0 = time.perf_counter()
+        sh1 = oshift.shift_coeffs(light_np[:1], shifts[:1], 2)
+        t_shift = time.perf_counter() - t0
+        i_s, v_s = synth.sparse_transfer_rows(cfg.seed, 0, rows, F, n, ks, dl)
+        Lb = np.broadcast_to(sh1.reshape(1, -1), (B, C))
+        t0 = time.perf_counter()
+        orelight.relight_sparse(i_s, v_s, Lb)
+        t_rel = time.perf_counter() - t0
+        full = t_shift * B + t_rel * (V / rows)
+        line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                                "sample": f"oracle fp64: shift of 1/{B} frames ({t_shift:.3f}s) + sparse relight of "
+                                          f"{rows}/{V} vertices x {B} frames ({t_rel:.3f}s), extrapolated linearly"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -965,17 +1003,38 @@ def run_rotate(args, cfg):
                              "trigonometry of the chain-rule kernel (SFU/ALU), not by HBM"},
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": None,
     }
+    if not args.no_e2e:
+        x_h = torch.from_numpy(maps_np).pin_memory()
+        y_h = torch.empty(y.shape, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            x.copy_(x_h, non_blocking=True)
+            step()
+            y_h.copy_(y, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.steps
+        line["e2e"] = {"value": B / (e_ms * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": int(maps_np.nbytes),
+                       "d2h_bytes_per_step": int(y.numel() * 4)}
     if not args.no_cpu_baseline:
         from oracle import rotate as orot
         yh = y.cpu().numpy()
-        k = 8
+        k = 1024   # a few seconds of oracle work
         t0 = time.perf_counter()
         refs = [orot.rotate_coeffs_chain(maps_np[b], *ang[b]) for b in range(k)]   # the parity oracle
         dt = time.perf_counter() - t0
         errs = [float(np.linalg.norm(yh[b] - refs[b]) / np.linalg.norm(refs[b])) for b in range(k)]
         line["parity_vs_oracle"] = {"max_rel_l2": max(errs), "maps": k, "tol": 1e-5}
-        ps = [orot.psnr(yh[b], orot.rotate_coeffs(maps_np[b], *ang[b])) for b in range(k)]
-        line["psnr_vs_spatial_db"] = {"min": min(ps), "median": float(np.median(ps)), "maps": k}
+        ps = [orot.psnr(yh[b], orot.rotate_coeffs(maps_np[b], *ang[b])) for b in range(16)]
+        line["psnr_vs_spatial_db"] = {"min": min(ps), "median": float(np.median(ps)), "maps": 16}
         line["cpu_baseline"] = {"value": k / dt, "unit": "maps/s", "cores": cpu_threads(), "kind": "oracle",
                                 "sample": f"oracle fp64 chain-rule rotation of {k}/{B} maps ({dt:.3f}s)"}
     print(json.dumps(line), flush=True)
