@@ -103,3 +103,21 @@ class ShiftTripleRelightPipeline(ShiftRelightPipeline):
     def _relight_chunk(self, s: int, n: int) -> None:
         api.relight_vertices_triple(self.T[s:s + n], self.vis[s:s + n], self.shifted, self.faces, self.k_face,
                                     out=self.R[s:s + n], workspace=self.tws, stream=self.compute)
+
+
+class ShiftSparseRelightPipeline(ShiftRelightPipeline):
+    """The same host pipeline with the sparse-transfer relight (row f2): per-vertex (index, value)
+    pairs over the full shifted pyramids (``relight_vertices_sparse``).  Each chunk's call
+    re-transposes the light (a ~0.03 ms pass at c5s), so fewer, larger chunks are used."""
+
+    def __init__(self, indices: torch.Tensor, values: torch.Tensor, faces: int, log2n: int, batch: int,
+                 chunks: int = 4):
+        super().__init__(values, faces, log2n, batch, log2n, chunks, full_pyramids=True)
+        self.rws = None   # the dense relight's workspace is not used here
+        self.idx = indices
+        need = api.relight_sparse_workspace_bytes(faces * (1 << (2 * log2n)), batch)
+        self.sws = torch.empty(need, dtype=torch.uint8, device=values.device)
+
+    def _relight_chunk(self, s: int, n: int) -> None:
+        api.relight_vertices_sparse(self.idx[s:s + n], self.T[s:s + n], self.shifted, out=self.R[s:s + n],
+                                    workspace=self.sws, stream=self.compute)

@@ -69,3 +69,29 @@ def test_sparse_shapes(faces, n, B, ks):
                                    torch.from_numpy(light).cuda()).cpu().numpy()
     ref = orelight.relight_sparse(idx, val, light.reshape(B, -1))
     assert np.linalg.norm(R - ref) / np.linalg.norm(ref) <= TOL
+
+
+def test_sparse_host_pipeline_matches_device_calls():
+    """ShiftSparseRelightPipeline (host buffers, chunked D2H under the next chunk's relight) returns
+    exactly the device path's radiance, step after step"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    from paper_1705_07272_b200.pipeline import ShiftSparseRelightPipeline
+    n, F, B, V, ks = 5, 6, 64, 1001, 128
+    idx = torch.empty((V, ks), dtype=torch.int32, device="cuda")
+    val = torch.empty((V, ks), dtype=torch.float32, device="cuda")
+    hs.hs_fill_sparse_transfer(idx, val, 0, F, n, 2, 33)
+    pipe = ShiftSparseRelightPipeline(idx, val, F, n, B, chunks=3)
+    outs, refs = [], []
+    for step in range(3):
+        light = synth.light_pyramids(50 + step, B, F, n)
+        sh = np.random.default_rng(step).uniform(0, 32, size=(B, F, 2))
+        lh = torch.from_numpy(light).pin_memory()
+        rh = torch.empty((V, B), dtype=torch.float32).pin_memory()
+        pipe.step(lh, sh, rh)
+        outs.append(rh)
+        s = hs.haar_shift_coeffs(torch.from_numpy(light).cuda(), sh, 2)
+        refs.append(hs.relight_vertices_sparse(idx, val, s).cpu())
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
