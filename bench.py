@@ -1003,26 +1003,24 @@ def run_rotate(args, cfg):
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": None,
     }
     if not args.no_e2e:
+        # host buffers through pipeline.RotatePipeline: chunked, copies under the rotation
+        from paper_1705_07272_b200.pipeline import RotatePipeline
+        pipe = RotatePipeline(B, n, dev, chunks=4)
         x_h = torch.from_numpy(maps_np).pin_memory()
-        y_h = torch.empty(y.shape, dtype=torch.float32).pin_memory()
-
-        def e2e_step():
-            x.copy_(x_h, non_blocking=True)
-            step()
-            y_h.copy_(y, non_blocking=True)
-
+        y_h = torch.empty((B, NN), dtype=torch.float32).pin_memory()
         for _ in range(max(1, args.warmup)):
-            e2e_step()
+            pipe.step(x_h, ang, y_h)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            e2e_step()
+            done = pipe.step(x_h, ang, y_h)
+        stream.wait_event(done)
         b.record(stream)
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b) / args.steps
         line["e2e"] = {"value": B / (e_ms * 1e-3), "unit": "maps/s", "h2d_bytes_per_step": int(maps_np.nbytes),
-                       "d2h_bytes_per_step": int(y.numel() * 4)}
+                       "d2h_bytes_per_step": int(B * NN * 4), "path": "pipeline.RotatePipeline"}
     if not args.no_cpu_baseline:
         from oracle import rotate as orot
         yh = y.cpu().numpy()

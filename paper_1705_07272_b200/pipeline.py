@@ -121,3 +121,48 @@ class ShiftSparseRelightPipeline(ShiftRelightPipeline):
     def _relight_chunk(self, s: int, n: int) -> None:
         api.relight_vertices_sparse(self.idx[s:s + n], self.T[s:s + n], self.shifted, out=self.R[s:s + n],
                                     workspace=self.sws, stream=self.compute)
+
+
+class RotatePipeline:
+    """Host-buffer rotation of lat-long maps (row f1): the maps are processed in chunks, chunk k+1's
+    H2D and chunk k-1's D2H (two copy streams, two copy engines) running under chunk k's
+    ``haar_rotate_coeffs``.  Plumbing only."""
+
+    def __init__(self, maps: int, log2n: int, device, chunks: int = 4):
+        self.N2 = 1 << (2 * log2n)
+        self.log2n = log2n
+        self.chunks = chunk_bounds(maps, chunks)
+        self.x = torch.empty((maps, self.N2), dtype=torch.float32, device=device)
+        self.y = torch.empty_like(self.x)
+        rows = max(n for _, n in self.chunks)
+        self.ws = torch.empty(api.haar_rotate_workspace_bytes(log2n, rows), dtype=torch.uint8, device=device)
+        self.compute = torch.cuda.current_stream(device)
+        self.h2d = torch.cuda.Stream(device)
+        self.d2h = torch.cuda.Stream(device)
+        self.ev_in = [torch.cuda.Event() for _ in self.chunks]
+        self.ev_done = [torch.cuda.Event() for _ in self.chunks]
+        self.ev_out = [torch.cuda.Event() for _ in self.chunks]
+        self.i = 0
+
+    def step(self, maps_host: torch.Tensor, angles, out_host: torch.Tensor) -> torch.cuda.Event:
+        """Enqueue one call; returns an event that completes when out_host holds the result."""
+        ang = np.asarray(angles, dtype=np.float64).reshape(-1, 2)
+        for c, (s, n) in enumerate(self.chunks):
+            with torch.cuda.stream(self.h2d):
+                if self.i >= 1:
+                    self.h2d.wait_event(self.ev_done[c])   # the previous call's rotation read x[s:s+n]
+                self.x[s:s + n].copy_(maps_host[s:s + n], non_blocking=True)
+                self.ev_in[c].record(self.h2d)
+        for c, (s, n) in enumerate(self.chunks):
+            self.compute.wait_event(self.ev_in[c])
+            if self.i >= 1:
+                self.compute.wait_event(self.ev_out[c])    # the previous call's D2H of y[s:s+n] is done
+            api.haar_rotate_coeffs(self.x[s:s + n], ang[s:s + n], out=self.y[s:s + n], workspace=self.ws,
+                                   stream=self.compute)
+            self.ev_done[c].record(self.compute)
+            self.d2h.wait_event(self.ev_done[c])
+            with torch.cuda.stream(self.d2h):
+                out_host[s:s + n].copy_(self.y[s:s + n], non_blocking=True)
+                self.ev_out[c].record(self.d2h)
+        self.i += 1
+        return self.ev_out[-1]

@@ -112,3 +112,19 @@ def test_parity_with_chain_rule_oracle(n, kind):
         err = _rel(got[b], ref)
         print(n, kind, b, ang[b], err)
         assert err <= 1e-5, (n, kind, b, ang[b], err)
+
+
+def test_rotate_host_pipeline_matches_device_call():
+    import torch
+    import paper_1705_07272_b200 as hs
+    from paper_1705_07272_b200.pipeline import RotatePipeline
+    n, B = 5, 37
+    pipe = RotatePipeline(B, n, torch.device("cuda"), chunks=3)
+    for step in range(2):
+        c = synth.smooth_sphere_maps(60 + step, B, n)
+        ang = synth.rotation_angles(61 + step, B)
+        xh = torch.from_numpy(c).pin_memory()
+        yh = torch.empty((B, 4 ** n), dtype=torch.float32).pin_memory()
+        pipe.step(xh, ang, yh).synchronize()
+        ref = hs.haar_rotate_coeffs(torch.from_numpy(c).cuda(), ang).cpu()
+        assert torch.equal(yh, ref)
