@@ -51,37 +51,37 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // ------------------------------------------------------------------------------- (1) top-down
 // level l -> l+1 for all maps: fields [map][2][4^l] (X, Y) in cur, [map][2][4^(l+1)] in nxt.
 __global__ void rot_topdown_kernel(const float* __restrict__ in, long long maps, int n, int l,
-                                   const float* __restrict__ cur, float* __restrict__ nxt) {
+                                   const double* __restrict__ cur, double* __restrict__ nxt) {
   const int g = 1 << l, G2 = 2 * g;
   const long long per = 1ll << (2 * l);
   const long long total = maps * per;
   const long long NN = 1ll << (2 * n);
-  const float asc = pow2f(l);
+  const double asc = (double)pow2f(l);
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long b = e >> (2 * l);
     const int cell = (int)(e & (per - 1));
     const int i = cell >> l, j = cell & (g - 1);
     const float* src = in + b * NN;
-    float d[3][4];  // cells (i,j), (i,j+1), (i+1,j): delta_00, delta_01, delta_10, delta_11
+    double d[3][4];  // cells (i,j), (i,j+1), (i+1,j): delta_00, delta_01, delta_10, delta_11
     const int cells[3] = {cell, i * g + ((j + 1) & (g - 1)), ((i + 1) & (g - 1)) * g + j};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const float H = __ldg(src + per + cells[k]) * asc;
-      const float V = __ldg(src + 2 * per + cells[k]) * asc;
-      const float D = __ldg(src + 3 * per + cells[k]) * asc;
+      const double H = (double)__ldg(src + per + cells[k]) * asc;
+      const double V = (double)__ldg(src + 2 * per + cells[k]) * asc;
+      const double D = (double)__ldg(src + 3 * per + cells[k]) * asc;
       d[k][0] = H + V + D;
       d[k][1] = -H + V - D;
       d[k][2] = H - V - D;
       d[k][3] = -H - V + D;
     }
-    float Xl = 0.f, Yl = 0.f;
+    double Xl = 0.0, Yl = 0.0;
     if (l > 0) {
       Xl = cur[b * 2 * per + cell];
       Yl = cur[b * 2 * per + per + cell];
     }
-    float* X = nxt + b * 8 * per;          // [2][4 per]
-    float* Y = X + 4 * per;
+    double* X = nxt + b * 8 * per;          // [2][4 per]
+    double* Y = X + 4 * per;
     const int r0 = 2 * i, c0 = 2 * j;
     // X[2i+a][2j] = d_a0 - d_a1 ;  X[2i+a][2j+1] = X_l + d_a1 - d_a0(i, j+1)
     X[r0 * G2 + c0] = d[0][0] - d[0][1];
@@ -156,25 +156,25 @@ __device__ __forceinline__ void rotated_kf(const Trig& tr, int kt, int kp, float
 
 // bilinear sample of a field plane (rows 0..R-1) extended by the reflected rows lo (row -1) and
 // hi (row R) at index coordinates (y, x), periodic in x
-__device__ __forceinline__ double sample_ext(const float* __restrict__ P, const float* __restrict__ lo,
-                                            const float* __restrict__ hi, int N, int R, double y, double x) {
+__device__ __forceinline__ double sample_ext(const double* __restrict__ P, const double* __restrict__ lo,
+                                            const double* __restrict__ hi, int N, int R, double y, double x) {
   y = fmin(fmax(y, -1.0), (double)R);
   const double fy = floor(y), fx = floor(x);
   const double wy = y - fy, wx = x - fx;
   const int y0 = (int)fy, y1 = min(y0 + 1, R);
   const int x0 = ((int)fx) & (N - 1), x1 = (x0 + 1) & (N - 1);
-  const float* r0 = y0 < 0 ? lo : (y0 >= R ? hi : P + y0 * N);
-  const float* r1 = y1 < 0 ? lo : (y1 >= R ? hi : P + y1 * N);
-  return (1.0 - wy) * ((1.0 - wx) * (double)__ldg(r0 + x0) + wx * (double)__ldg(r0 + x1)) +
-         wy * ((1.0 - wx) * (double)__ldg(r1 + x0) + wx * (double)__ldg(r1 + x1));
+  const double* r0 = y0 < 0 ? lo : (y0 >= R ? hi : P + y0 * N);
+  const double* r1 = y1 < 0 ? lo : (y1 >= R ? hi : P + y1 * N);
+  return (1.0 - wy) * ((1.0 - wx) * __ldg(r0 + x0) + wx * __ldg(r0 + x1)) +
+         wy * ((1.0 - wx) * __ldg(r1 + x0) + wx * __ldg(r1 + x1));
 }
 
 // pole rows per map: E [map][4][N] = X row -1, X row N, Y row -1, Y row N-1 (reflected)
-__global__ void rot_pole_kernel(const float* __restrict__ F, int n, float* __restrict__ E) {
+__global__ void rot_pole_kernel(const double* __restrict__ F, int n, double* __restrict__ E) {
   const int N = 1 << n, h = N / 2;
   const long long NN = 1ll << (2 * n);
-  const float* X = F + (long long)blockIdx.x * 2 * NN;
-  float* e = E + (long long)blockIdx.x * 4 * N;
+  const double* X = F + (long long)blockIdx.x * 2 * NN;
+  double* e = E + (long long)blockIdx.x * 4 * N;
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
     e[c] = X[(c + h) & (N - 1)];                              // X(theta_-1, phi) = X(theta_0, phi + pi)
     e[N + c] = X[(N - 1) * N + ((c + h) & (N - 1))];
@@ -193,9 +193,9 @@ __global__ void rot_pole_kernel(const float* __restrict__ F, int n, float* __res
 // +1 halo (row and column) are computed once into shared memory, so each pixel costs three fp64
 // rotations (its centre, shared with two neighbours' differences, and two midpoints) instead of five.
 constexpr int kTS = 16;
-__global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const float* __restrict__ F, const float* __restrict__ E,
+__global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const double* __restrict__ F, const double* __restrict__ E,
                                                                   int n, const __grid_constant__ RotParams prm, Trig tr,
-                                                                  float* __restrict__ Gf) {
+                                                                  double* __restrict__ Gf) {
   __shared__ Ang C[kTS + 1][kTS + 1];
   const int N = 1 << n;
   const int TS = N < kTS ? N : kTS;
@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const float* _
   const int ti = threadIdx.x / TS, tj = threadIdx.x - ti * TS;
   const int i = i0 + ti, j = j0 + tj;
   const double iT = (double)N / 3.141592653589793, iP = (double)N / 6.283185307179586;
-  const float* Xf = F + (long long)b * 2 * NN;
-  const float* Yf = Xf + NN;
-  const float* Eb = E + (long long)b * 4 * N;
+  const double* Xf = F + (long long)b * 2 * NN;
+  const double* Yf = Xf + NN;
+  const double* Eb = E + (long long)b * 4 * N;
   const Ang A0 = C[ti][tj];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
@@ -230,28 +230,28 @@ __global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const float* _
     double dP = A0.Ph - A1.Ph;
     if (dP > 3.141592653589793) dP -= 6.283185307179586;
     if (dP < -3.141592653589793) dP += 6.283185307179586;
-    Gf[(long long)b * 2 * NN + t * NN + (long long)i * N + j] = (float)(-yf * dT * iT - xf * dP * iP);
+    Gf[(long long)b * 2 * NN + t * NN + (long long)i * N + j] = -yf * dT * iT - xf * dP * iP;
   }
 }
 
 // closure: rows of X_g sum to 0 (subtract the row mean); column j of Y_g: last row = -sum of the
 // others.  One CTA per map; a warp per row (coalesced), a thread per column (coalesced).
-__global__ void rot_closure_kernel(float* __restrict__ Gf, int n) {
+__global__ void rot_closure_kernel(double* __restrict__ Gf, int n) {
   const int N = 1 << n;
   const long long NN = 1ll << (2 * n);
-  float* X = Gf + (long long)blockIdx.x * 2 * NN;
-  float* Y = X + NN;
+  double* X = Gf + (long long)blockIdx.x * 2 * NN;
+  double* Y = X + NN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = warp; r < N; r += nw) {
-    float sx = 0.f;
+    double sx = 0.0;
     for (int t = lane; t < N; t += 32) sx += X[r * N + t];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    const float mx = sx / (float)N;
+    const double mx = sx / (double)N;
     for (int t = lane; t < N; t += 32) X[r * N + t] -= mx;
   }
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    float sy = 0.f;
+    double sy = 0.0;
     for (int t = 0; t < N - 1; ++t) sy += Y[t * N + k];
     Y[(N - 1) * N + k] = -sy;
   }
@@ -260,21 +260,21 @@ __global__ void rot_closure_kernel(float* __restrict__ Gf, int n) {
 // ------------------------------------------------------------------------------- (3) bottom-up
 // from fields at level l+1 (src: [map][planes][4^(l+1)]; at the finest level planes = 2 and
 // Z = X[i] - X[i+1]) to level l (dst [map][3][4^l]) and the level-l details of the output pyramid.
-__global__ void rot_bottomup_kernel(const float* __restrict__ src, int src_planes, long long maps, int l,
-                                    float* __restrict__ dst, float* __restrict__ out, int n) {
+__global__ void rot_bottomup_kernel(const double* __restrict__ src, int src_planes, long long maps, int l,
+                                    double* __restrict__ dst, float* __restrict__ out, int n) {
   const int g = 1 << l, G2 = 2 * g;
   const long long per = 1ll << (2 * l), sper = 4 * per;
   const long long total = maps * per;
   const long long NN = 1ll << (2 * n);
-  const float q = 0.25f, osc = pow2f(-l);
+  const double q = 0.25, osc = (double)pow2f(-l);
   const bool zfromx = (src_planes == 2);
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long b = e >> (2 * l);
     const int cell = (int)(e & (per - 1));
     const int i = cell >> l, j = cell & (g - 1);
-    const float* X = src + b * src_planes * sper;
-    const float* Y = X + sper;
+    const double* X = src + b * src_planes * sper;
+    const double* Y = X + sper;
     const int rr[4] = {2 * i, 2 * i + 1, (2 * i + 2) & (G2 - 1), (2 * i + 3) & (G2 - 1)};
     const int cc[3] = {2 * j, 2 * j + 1, (2 * j + 2) & (G2 - 1)};
     auto x = [&](int u, int w) { return X[rr[u] * G2 + cc[w]]; };
@@ -282,18 +282,18 @@ __global__ void rot_bottomup_kernel(const float* __restrict__ src, int src_plane
     auto z = [&](int u, int w) {
       return zfromx ? X[rr[u] * G2 + cc[w]] - X[rr[u + 1] * G2 + cc[w]] : X[2 * sper + rr[u] * G2 + cc[w]];
     };
-    const float Xn = q * (x(0, 0) + 2.f * x(0, 1) + x(0, 2) + x(1, 0) + 2.f * x(1, 1) + x(1, 2));
-    const float Yn = q * (y(0, 0) + 2.f * y(1, 0) + y(2, 0) + y(0, 1) + 2.f * y(1, 1) + y(2, 1));
-    const float Zn = q * ((z(0, 0) + 2.f * z(0, 1) + z(0, 2)) + 2.f * (z(1, 0) + 2.f * z(1, 1) + z(1, 2)) +
-                          (z(2, 0) + 2.f * z(2, 1) + z(2, 2)));
-    float* D = dst + b * 3 * per;
+    const double Xn = q * (x(0, 0) + 2.0 * x(0, 1) + x(0, 2) + x(1, 0) + 2.0 * x(1, 1) + x(1, 2));
+    const double Yn = q * (y(0, 0) + 2.0 * y(1, 0) + y(2, 0) + y(0, 1) + 2.0 * y(1, 1) + y(2, 1));
+    const double Zn = q * ((z(0, 0) + 2.0 * z(0, 1) + z(0, 2)) + 2.0 * (z(1, 0) + 2.0 * z(1, 1) + z(1, 2)) +
+                          (z(2, 0) + 2.0 * z(2, 1) + z(2, 2)));
+    double* D = dst + b * 3 * per;
     D[cell] = Xn;
     D[per + cell] = Yn;
     D[2 * per + cell] = Zn;
     float* o = out + b * NN;
-    o[per + cell] = q * (x(0, 0) + x(1, 0)) * osc;
-    o[2 * per + cell] = q * (y(0, 0) + y(0, 1)) * osc;
-    o[3 * per + cell] = q * z(0, 0) * osc;
+    o[per + cell] = (float)(q * (x(0, 0) + x(1, 0)) * osc);   // one rounding per output
+    o[2 * per + cell] = (float)(q * (y(0, 0) + y(0, 1)) * osc);
+    o[3 * per + cell] = (float)(q * z(0, 0) * osc);
   }
 }
 
@@ -368,32 +368,38 @@ unsigned grid_for(long long total) {
 
 }  // namespace
 
-// Workspace: F ping-pong 2 x [maps][2][N^2], G [maps][2][N^2], tmp pyramid [maps][N^2], pole rows
-// [maps][4][N], then the shift's workspace.
+// Workspace (fp64 fields: fp32 rounding of the fine differences is amplified on the coarse levels
+// the recursion sums): F ping-pong 2 x [chunk][2][N^2] doubles, G [chunk][2][N^2]
+// doubles, pole rows [chunk][4][N] doubles, the trig table, the pre-azimuth pyramids [maps][N^2]
+// fp32, then the shift's workspace (chunk = min(maps, 1024)).
 size_t rotate_workspace_bytes_impl(int log2n, long long maps) {
   const size_t NN = (size_t)1 << (2 * log2n);
-  const size_t f = (size_t)maps * NN * sizeof(float);
-  const size_t pb = ((size_t)maps * 4 * ((size_t)1 << log2n) * sizeof(float) + 255) & ~size_t(255);
+  const size_t mc = (size_t)(maps < kRotChunk ? maps : kRotChunk);
+  const size_t fd = (mc * 2 * NN * sizeof(double) + 255) & ~size_t(255);
+  const size_t pb = (mc * 4 * ((size_t)1 << log2n) * sizeof(double) + 255) & ~size_t(255);
   const size_t tb = (4 * (2 * ((size_t)1 << log2n) + 2) * sizeof(double) + 255) & ~size_t(255);
-  return 2 * 2 * f + 2 * f + f + pb + tb + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
+  const size_t tp = ((size_t)maps * NN * sizeof(float) + 255) & ~size_t(255);
+  return 3 * fd + pb + tb + tp + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
 }
 
 hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
                         size_t ws_bytes, cudaStream_t st) {
   const long long NN = 1ll << (2 * n);
-  const size_t f = (size_t)maps * NN * sizeof(float);
-  char* base = reinterpret_cast<char*>(ws);
-  float* bufA = reinterpret_cast<float*>(base);
-  float* bufB = reinterpret_cast<float*>(base + 2 * f);
-  float* Gf = reinterpret_cast<float*>(base + 4 * f);
-  float* tmp = reinterpret_cast<float*>(base + 6 * f);
-  const size_t pb = ((size_t)maps * 4 * ((size_t)1 << n) * sizeof(float) + 255) & ~size_t(255);
-  float* poles = reinterpret_cast<float*>(base + 7 * f);
+  const size_t mcap = (size_t)(maps < kRotChunk ? maps : kRotChunk);
+  const size_t fd = (mcap * 2 * (size_t)NN * sizeof(double) + 255) & ~size_t(255);
+  const size_t pb = (mcap * 4 * ((size_t)1 << n) * sizeof(double) + 255) & ~size_t(255);
   const int K = 2 * (1 << n) + 2;
   const size_t tb = (4 * (size_t)K * sizeof(double) + 255) & ~size_t(255);
-  double* tab = reinterpret_cast<double*>(base + 7 * f + pb);
-  void* sws = base + 7 * f + pb + tb;
-  const size_t sws_bytes = ws_bytes - 7 * f - pb - tb;
+  const size_t tp = ((size_t)maps * NN * sizeof(float) + 255) & ~size_t(255);
+  char* base = reinterpret_cast<char*>(ws);
+  double* bufA = reinterpret_cast<double*>(base);
+  double* bufB = reinterpret_cast<double*>(base + fd);
+  double* Gf = reinterpret_cast<double*>(base + 2 * fd);
+  double* poles = reinterpret_cast<double*>(base + 3 * fd);
+  double* tab = reinterpret_cast<double*>(base + 3 * fd + pb);
+  float* tmp = reinterpret_cast<float*>(base + 3 * fd + pb + tb);
+  void* sws = base + 3 * fd + pb + tb + tp;
+  const size_t sws_bytes = ws_bytes - (3 * fd + pb + tb + tp);
   rot_table_kernel<<<(K + 255) / 256, 256, 0, st>>>(n, tab);
   HS_CHECK_LAUNCH("rot_table_kernel");
   const Trig tr{tab, tab + K, tab + 2 * K, tab + 3 * K};
@@ -408,9 +414,9 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
     const float* src = in + m0 * NN;
     float* dtmp = tmp + m0 * NN;
     // (1) top-down to the finest fields (ping-pong between bufA and bufB)
-    float* cur = bufB;
+    double* cur = bufB;
     for (int l = 0; l < n; ++l) {
-      float* nxt = (cur == bufA) ? bufB : bufA;
+      double* nxt = (cur == bufA) ? bufB : bufA;
       rot_topdown_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(src, mc, n, l, cur, nxt);
       HS_CHECK_LAUNCH("rot_topdown_kernel");
       cur = nxt;
@@ -428,9 +434,9 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
     rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
     HS_CHECK_LAUNCH("rot_closure_kernel");
     // (3) bottom-up, every detail level of the rotated pyramid
-    const float* s = Gf;
+    const double* s = Gf;
     int planes = 2;
-    float* d = bufA;
+    double* d = bufA;
     for (int l = n - 1; l >= 0; --l) {
       rot_bottomup_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(s, planes, mc, l, d, dtmp, n);
       HS_CHECK_LAUNCH("rot_bottomup_kernel");

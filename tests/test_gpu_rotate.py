@@ -93,11 +93,12 @@ def test_psnr_against_spatial_and_analytic_ground_truth():
     assert res[5][2] < res[6][2] < res[7][2]
 
 
-@pytest.mark.parametrize("n,kind", [(3, "smooth"), (4, "noise"), (5, "smooth"), (6, "smooth"), (6, "noise"),
-                                    (7, "smooth")])
+@pytest.mark.parametrize("n,kind", [(1, "noise"), (2, "noise"), (3, "smooth"), (4, "noise"), (5, "smooth"),
+                                    (6, "smooth"), (6, "noise"), (7, "smooth"), (8, "smooth"), (9, "noise"),
+                                    (11, "noise")])
 def test_parity_with_chain_rule_oracle(n, kind):
     rng = np.random.default_rng(100 + n)
-    B = 6
+    B = 6 if n <= 9 else 3
     if kind == "smooth":
         c = synth.smooth_sphere_maps(20 + n, B, n)
     else:
