@@ -229,3 +229,19 @@ def test_relight_shifted_fuzz_n128(case):
     ref = orelight.relight_shifted(T, L, vs.astype(np.float64))
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert err <= 1e-5, (faces, V, err)
+
+
+@pytest.mark.parametrize("B", [1, 3, 64])
+def test_relight_dense_long_rows(B):
+    """the longest rows the ABI serves in practice: 6 faces x 4^8 = 393216 coefficients per vertex
+    (GEMV for small batches, the drained tensor-core chain for 64)"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    k, faces, V = 8, 6, 130
+    T = synth.transfer_rows(77, 0, V, faces, 4 ** k)
+    L = synth.light_pyramids(78, B, faces, k)
+    R = hs.relight_vertices(torch.from_numpy(T).cuda(), torch.from_numpy(L).cuda(), faces, 4 ** k).cpu().numpy()
+    ref = orelight.relight(T, L, faces, 4 ** k)
+    err = np.linalg.norm(R - ref) / np.linalg.norm(ref)
+    print(B, err)
+    assert err <= 1e-5, (B, err)
