@@ -35,9 +35,9 @@
 //   coarse_finish_kernel  one CTA per face: the coarse bottom-up c -> 0 from the shifted fields.
 // Levels >= m (dyadic shifts) are exact permutations (permute_kernel).
 //
-// Field precision FT: fp32 for log2n <= 7; fp64 above (DESIGN.md §4.1 error model: fine-level
-// fp32 rounding is amplified ~2^(n-l) on the coarse outputs of large faces; at N = 256 the
-// relight band of the c5 light reached 1.3e-5 per frame in fp32, 3e-8 in fp64).
+// Field precision: fp64 at every size (DESIGN.md §4.1 error model: fine-level fp32 rounding is
+// amplified ~2^(n-l) on the coarse outputs; at N = 256 the relight band of the c5 light reached
+// 1.3e-5 per frame in fp32, 3e-8 in fp64; white noise at N = 64 with a one-level band 2e-5).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -762,9 +762,130 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
   return HS_OK;
 }
 
+// Small faces (N <= 32): the whole shift of one face in one CTA -- the pyramid is read once into
+// shared memory (one global round trip instead of one per phase of the tile path), then the
+// top-down to the working level m, the shift at m, the bottom-up m -> 0 (coarse_finish) and the
+// permuted levels >= m, all in fp64 shared memory.  One launch per call.
+constexpr int kSmallMaxLog2n = 5;
+constexpr int kSmallSmem = (1 << (2 * kSmallMaxLog2n)) * 4 +                           // the pyramid
+                           (3 * (1 << (2 * kSmallMaxLog2n)) * 2 + 3 * (1 << (2 * (kSmallMaxLog2n - 1)))) * 8;
+
+__global__ void __launch_bounds__(kThreads) shift2d_small_kernel(const __grid_constant__ ShiftArgs args) {
+  extern __shared__ __align__(16) unsigned char ssm[];
+  const int g = blockIdx.x;
+  const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
+  const int n = args.log2n, m = P.m, band = args.band;
+  const int NN = 1 << (2 * n);
+  const int b = g / args.faces, f = g % args.faces;
+  const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
+  float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
+  float* C = reinterpret_cast<float*>(ssm);                       // the input pyramid
+  double* FA = reinterpret_cast<double*>(ssm + (size_t)NN * 4);   // 3 x 4^m
+  double* FB = FA + 3 * (1 << (2 * m));                           // 3 x 4^m
+  double* FC = FB + 3 * (1 << (2 * m));                           // 3 x 4^(m-1) (bottom-up scratch)
+  for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) C[idx] = __ldg(in + idx);
+  __syncthreads();
+  // levels >= m (up to the band): exact permutations; the scaling coefficient is shift invariant
+  const int hi = 1 << (2 * band);
+  for (int idx = threadIdx.x; idx < hi; idx += blockDim.x) {
+    if (idx == 0) {
+      out[0] = C[0];
+      continue;
+    }
+    const int l = (31 - __clz(idx)) >> 1;
+    if (l < m) continue;
+    const int base = 1 << (2 * l), r = idx - base, t = r >> (2 * l), cell = r & (base - 1);
+    const int i = cell >> l, j = cell & ((1 << l) - 1), sh = n - l;
+    const int si = (i - (P.qy >> sh)) & ((1 << l) - 1), sj = (j - (P.qx >> sh)) & ((1 << l) - 1);
+    out[idx] = C[base * (1 + t) + (si << l) + sj];
+  }
+  if (m == 0) return;
+  // top-down: fields of levels 1 .. m (X, Y, Z), ping-pong FA / FB, level m ends in FA
+  for (int l = 0; l < m; ++l) {
+    const int gl = 1 << l, G2 = 2 * gl;
+    const double asc = (double)pow2f(l);
+    const double* cur = ((m - l) & 1) ? FB : FA;
+    double* nxt = ((m - l - 1) & 1) ? FB : FA;
+    for (int idx = threadIdx.x; idx < gl * gl; idx += blockDim.x) {
+      const int i = idx >> l, j = idx & (gl - 1);
+      double d[2][2][2][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int o = ((i + u) & (gl - 1)) * gl + ((j + v) & (gl - 1));
+          const double H = (double)C[gl * gl * 1 + o] * asc;
+          const double V = (double)C[gl * gl * 2 + o] * asc;
+          const double D = (double)C[gl * gl * 3 + o] * asc;
+          d[u][v][0][0] = H + V + D;
+          d[u][v][0][1] = -H + V - D;
+          d[u][v][1][0] = H - V - D;
+          d[u][v][1][1] = -H - V + D;
+        }
+      double Xl = 0.0, Yl = 0.0, Zl = 0.0;
+      if (l > 0) {
+        Xl = cur[idx];
+        Yl = cur[gl * gl + idx];
+        Zl = cur[2 * gl * gl + idx];
+      }
+      double cx[2][2], cy[2][2], cz[2][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        cx[a][0] = d[0][0][a][0] - d[0][0][a][1];
+        cx[a][1] = Xl + d[0][0][a][1] - d[0][1][a][0];
+      }
+#pragma unroll
+      for (int bq = 0; bq < 2; ++bq) {
+        cy[0][bq] = d[0][0][0][bq] - d[0][0][1][bq];
+        cy[1][bq] = Yl + d[0][0][1][bq] - d[1][0][0][bq];
+      }
+      cz[0][0] = d[0][0][0][0] - d[0][0][0][1] - d[0][0][1][0] + d[0][0][1][1];
+      cz[0][1] = d[0][0][0][1] - d[0][0][1][1] - d[0][1][0][0] + d[0][1][1][0];
+      cz[1][0] = d[0][0][1][0] - d[0][0][1][1] - d[1][0][0][0] + d[1][0][0][1];
+      cz[1][1] = Zl + d[0][0][1][1] - d[0][1][1][0] - d[1][0][0][1] + d[1][1][0][0];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bq = 0; bq < 2; ++bq) {
+          const int o = (2 * i + a) * G2 + (2 * j + bq);
+          nxt[o] = cx[a][bq];
+          nxt[G2 * G2 + o] = cy[a][bq];
+          nxt[2 * G2 * G2 + o] = cz[a][bq];
+        }
+    }
+    __syncthreads();
+  }
+  // the shift at level m: box projection with weights (1 - phi, phi) on offsets Q, Q + 1
+  const int gm = 1 << m, GM = gm * gm;
+  const double wy1 = (double)P.wy, wx1 = (double)P.wx, wy0 = 1.0 - wy1, wx0 = 1.0 - wx1;
+  for (int idx = threadIdx.x; idx < 3 * GM; idx += blockDim.x) {
+    const int fl = idx / GM, cell = idx - fl * GM, y = cell >> m, x = cell & (gm - 1);
+    const double* F = FA + fl * GM;
+    const int y0 = (y - P.Qy) & (gm - 1), y1 = (y - P.Qy - 1) & (gm - 1);
+    const int x0 = (x - P.Qx) & (gm - 1), x1 = (x - P.Qx - 1) & (gm - 1);
+    FB[idx] = wy0 * (wx0 * F[y0 * gm + x0] + wx1 * F[y0 * gm + x1]) + wy1 * (wx0 * F[y1 * gm + x0] + wx1 * F[y1 * gm + x1]);
+  }
+  __syncthreads();
+  // bottom-up m -> 0 (details of levels < band)
+  coarse_finish<double>(FB, FC, FA, m, out, band, false);
+}
+
 }  // namespace
 
 hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, cudaStream_t st) {
+  if (a.log2n <= kSmallMaxLog2n) {
+    const size_t smem = (size_t)(1 << (2 * a.log2n)) * 4 +
+                        ((size_t)3 * (1 << (2 * a.log2n)) * 2 + 3 * (1 << (2 * (a.log2n > 0 ? a.log2n - 1 : 0)))) * 8;
+    static bool attr = false;
+    if (!attr) {
+      HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmem),
+                    "cudaFuncSetAttribute(shift2d_small_kernel)");
+      attr = true;
+    }
+    shift2d_small_kernel<<<a.num_faces, kThreads, smem, st>>>(a);
+    HS_CHECK_LAUNCH("shift2d_small_kernel");
+    return HS_OK;
+  }
   if (max_tiles > 0) {
     // fp64 fields at every size: fp32 rounding in the difference fields is amplified ~2^(n-l) on a
     // band of level l; the randomised sweep (tests/test_gpu_fuzz.py) measured
