@@ -158,6 +158,9 @@ HS_API size_t relight_workspace_bytes(int faces, int k_face, int batch);
  *   vertex_shifts  DEVICE pointer [num_vertices][2] fp32 (sy, sx), finite.
  *   radiance       [num_vertices] fp32.
  *   workspace      >= relight_shifted_workspace_bytes(...) bytes.
+ * Paths: N = 32, 64 fused per-vertex stencil; N = 128 residue planes of the light (exact: the box
+ * shift is four integer rolls and the bottom-up commutes with even rolls);
+ * larger N the chunked tile shift + row dot.  The light's fields are built in fp64.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, int faces,
                                    const float* light, int log2n, const float* vertex_shifts,
@@ -253,9 +256,10 @@ HS_API hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64
  *                 columns (f'(x) = f(x - s), exact, as haar_shift_coeffs).
  *   log2n         1 .. 11.   workspace >= haar_rotate_workspace_bytes(log2n, batch), 16-byte aligned.
  *   Accuracy: the elevation is the paper's first-order chain rule on the finest-level difference
- *   fields with bilinear resampling (approximate by construction: compared with the spatial
- *   ground truth as PSNR, R25-R27); alpha = 0 reproduces the input to fp32 rounding
- *   and the azimuth part is exact.
+ *   fields with bilinear resampling (R25-R27), computed with fp64 angles and fp64
+ *   fields and rounded once to fp32: it equals the fp64 oracle of that algorithm to ~1e-7
+ *   relative; against the spatial rotation it is approximate by construction (PSNR, improving
+ *   with N).  alpha = 0 reproduces the input to fp32 rounding and the azimuth part is exact.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status haar_rotate_coeffs(const float* in, float* out, int log2n, int batch, const double* angles_host,
                                     void* workspace, size_t workspace_bytes, void* stream);
