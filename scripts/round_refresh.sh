@@ -3,7 +3,7 @@
 #   every bench config's JSON line, the c5 launch list, ncu --set full of the dominant kernels
 #   (c5: relight_tc + shift tile; c4: residue-plane kernels; c5s: vectorised gather), parity margins.
 set -u
-TAG=${1:-r01f}
+TAG=${1:-r01g}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 for c in c5 c2 c3 c4 c5s c5t c5x c6r; do
