@@ -420,6 +420,8 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": V / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "arithmetic": "fp32 in / out; shift fields fp64; relight: fp32 GEMV (B <= 8) or tcgen05 products of "
+                          "fp16 hi/lo splits accumulated in fp32 (B % 64 == 0), within 1e-5 of the fp64 oracle",
             "config": {**workload_config(cfg, world), "gather": gather_mode},
             "vertex_frames_per_sec": V * B / (ms_max * 1e-3),
             "shift_coeffs_per_sec": B * F * N * N / (ms_max * 1e-3),
