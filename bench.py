@@ -594,7 +594,7 @@ def run_aux(args, cfg):
             hs.relight_vertices(T, shifted, F, kf, out=R)
             launches["n"] += hs.last_launch_count()
         graph_launches = launches["n"] - n0
-        kernel_name = "shift + relight (one CUDA graph replay: 4 kernels)"
+        kernel_name = f"shift + relight (one CUDA graph replay: {graph_launches} kernels)"
         stream.wait_stream(s_cap)
         for i in range(2):
             graph.replay()
