@@ -245,3 +245,18 @@ def test_relight_dense_long_rows(B):
     err = np.linalg.norm(R - ref) / np.linalg.norm(ref)
     print(B, err)
     assert err <= 1e-5, (B, err)
+
+
+@pytest.mark.parametrize("n,band,sh", [(12, 4, (1234.375, -77.25)), (11, 11, (0.5, 1023.0)), (10, 6, (512.0, 256.0))])
+def test_shift_largest_faces(n, band, sh):
+    """the largest faces the ABI takes (HS_MAX_LOG2N = 12: 4096^2), white noise, fractional /
+    half / dyadic shifts, band or full pyramid"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    N = 1 << n
+    c = synth.random_signals(90 + n, 1, N * N).reshape(1, 1, N * N)
+    got = hs.haar_shift_coeffs(torch.from_numpy(np.ascontiguousarray(c, dtype=np.float32)).cuda(),
+                               np.array([[list(sh)]]), 2, band).cpu().numpy()
+    ref = oshift.shift_coeffs(c, np.array([[list(sh)]]), 2, band_levels=band)
+    err = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    assert err <= 1e-5, (n, band, err)
