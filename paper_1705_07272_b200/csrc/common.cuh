@@ -156,6 +156,10 @@ hs_status launch_rowdot(const float* T, const float* S, long long rows, long lon
 bool relight_shifted_fused_supported(int log2n);
 size_t relight_shifted_fused_workspace_bytes(long long V, int faces, int log2n);
 size_t relight_planes_workspace_bytes(long long V, int faces);
+size_t relight_small_planes_workspace_bytes(long long V, int faces, int log2n);
+hs_status launch_relight_small_planes(const float* T, long long V, int faces, const float* light, int log2n,
+                                      const double* fields64, long long face_stride, const int4* vparams, float* R,
+                                      void* ws, cudaStream_t st);
 hs_status launch_relight_planes(const float* T, long long V, int faces, const float* light, const double* fields64,
                                 long long face_stride, const int4* vparams, float* R, void* ws, cudaStream_t st);
 hs_status launch_relight_shifted_fused(const float* T, long long V, int faces, const float* light, int log2n,

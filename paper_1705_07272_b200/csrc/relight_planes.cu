@@ -347,6 +347,186 @@ int sm_count() {
   return n;
 }
 
+// ------------------------------------------------------------------------------- N <= 64: every level
+// For small faces every level's residue planes fit in shared memory at once (n levels x 4^n
+// values: 96 KB at N = 64), so the per-vertex work is only rolled plane reads:
+//   r_v(unit) = sum_l sum_ab w_ab < T_l, roll(D_{l, Q_ab mod 2^(n-l)}, Q_ab div 2^(n-l)) >
+// with no shift, no stencil and no bottom-up per vertex.  D_l layout per unit and level:
+// [rho_y][rho_x][2^l][2^l] (4^n floats), levels n-1 .. 0 concatenated.
+
+// residue planes of every level of one (face, field), fp64 recursion in shared memory
+template <int FLD>
+__device__ void small_planes_body(const double* F, int n, float* out, double* A, double* Bf) {
+  const int NN = 1 << (2 * n);
+  const double* src = F;   // level n fields (one residue)
+  double* dst = A;
+  for (int k = 1; k <= n; ++k) {
+    const int l = n - k, g = 1 << l, gg = g * g, R = 1 << k;       // output level, side, residues per axis
+    const int Gs = 2 * g, Rp = R >> 1;                             // source side, source residues per axis
+    float* D = out + (long long)(k - 1) * NN;
+    for (int idx = threadIdx.x; idx < NN; idx += blockDim.x) {
+      const int rho = idx / gg, cell = idx - rho * gg;
+      const int ry = rho / R, rx = rho - ry * R;
+      const int i = cell >> l, j = cell & (g - 1);
+      const double* S = src + (long long)((ry % Rp) * Rp + (rx % Rp)) * (Gs * Gs);
+      double fv, dv;
+      bu_rolled<double, FLD>(S, Gs, i, j, ry / Rp, rx / Rp, fv, dv);
+      dst[idx] = fv;
+      D[idx] = (float)(dv * (double)pw2(-l));
+    }
+    __syncthreads();
+    src = dst;
+    dst = (dst == A) ? Bf : A;
+  }
+}
+
+__global__ void __launch_bounds__(512) small_planes_kernel(const double* __restrict__ fields64, long long face_stride,
+                                                           int n, float* __restrict__ planes) {
+  extern __shared__ double sp[];   // two 4^n ping-pong planes (fp64)
+  const int f = blockIdx.x / 3, t = blockIdx.x % 3;
+  const int NN = 1 << (2 * n);
+  const double* F = fields64 + (long long)f * face_stride + (long long)t * NN;
+  float* out = planes + (long long)blockIdx.x * n * NN;
+  if (t == 0) small_planes_body<0>(F, n, out, sp, sp + NN);
+  else if (t == 1) small_planes_body<1>(F, n, out, sp, sp + NN);
+  else small_planes_body<2>(F, n, out, sp, sp + NN);
+}
+
+constexpr int kSWarps = 32;
+
+template <int LOG2N>
+__global__ void __launch_bounds__(kSWarps * 32)
+    small_relight_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ planes,
+                         const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
+  constexpr int n = LOG2N, NN = 1 << (2 * n);
+  extern __shared__ __align__(16) float Ds[];   // [n][4^n]: levels n-1 .. 0
+  const int units = 3 * faces;
+  const int unit = blockIdx.x % units, split = blockIdx.x / units;
+  const int f = unit / 3, t = unit - 3 * (unit / 3);
+  const float* src = planes + (long long)unit * n * NN;
+  for (int idx = threadIdx.x; idx < n * NN; idx += blockDim.x) Ds[idx] = __ldg(src + idx);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long Kt = (long long)faces * NN;
+  const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
+  for (long long v = v0 + warp; v < v1; v += kSWarps) {
+    const int4 pr = __ldg(vparams + v);
+    const float* Tv = T + v * Kt + (long long)f * NN;
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+    for (int k = 1; k <= n; ++k) {
+      const int l = n - k, g = 1 << l, gg = g * g, R = 1 << k;
+      const float* D = Ds + (k - 1) * NN;
+      const float* Tl = Tv + (long long)(1 + t) * gg;
+      int ry[2], rx[2], py[2], px[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int Qy = (pr.x + a) & ((1 << n) - 1), Qx = (pr.y + a) & ((1 << n) - 1);
+        py[a] = Qy & (R - 1);
+        ry[a] = Qy >> k;
+        px[a] = Qx & (R - 1);
+        rx[a] = Qx >> k;
+      }
+      const float* Db[2][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) Db[a][b] = D + (py[a] * R + px[b]) * gg;
+#pragma unroll 8   // T loads of several cells in flight (the HBM latency, not the arithmetic, bounds this)
+      for (int idx = lane; idx < gg; idx += 32) {
+        const int i = idx >> l, j = idx & (g - 1);
+        const float tv = __ldg(Tl + idx);
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int row = (i - ry[a]) & (g - 1);
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const float d = Db[a][b][row * g + ((j - rx[b]) & (g - 1))];
+            acc[a][b] = fmaf(tv, d, acc[a][b]);
+          }
+        }
+      }
+    }
+    const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
+    float r = wy0 * (wx0 * acc[0][0] + wx1 * acc[0][1]) + wy1 * (wx0 * acc[1][0] + wx1 * acc[1][1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0) partial[v * units + unit] = r;
+  }
+}
+
+__global__ void small_finish_kernel(const float* __restrict__ partial, const float* __restrict__ T,
+                                    const float* __restrict__ light, long long V, int faces, int n,
+                                    float* __restrict__ R) {
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int units = 3 * faces;
+  const long long NN = 1ll << (2 * n);
+  float s = 0.f;
+  for (int u = 0; u < units; ++u) s += partial[v * units + u];
+  for (int f = 0; f < faces; ++f) s = fmaf(__ldg(T + v * faces * NN + f * NN), __ldg(light + f * NN), s);
+  R[v] = s;
+}
+
+template <int LOG2N>
+hs_status launch_small_relight(const float* T, long long V, int faces, const float* planes, const int4* vparams,
+                               float* partial, cudaStream_t st) {
+  constexpr int SM = LOG2N * (1 << (2 * LOG2N)) * 4;
+  static bool attr = false;
+  if (!attr) {
+    HS_CHECK_CUDA(cudaFuncSetAttribute(small_relight_kernel<LOG2N>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM),
+                  "cudaFuncSetAttribute(small_relight_kernel)");
+    attr = true;
+  }
+  const int units = 3 * faces;
+  const int per_sm = (227 * 1024) / (SM + 1024) >= 2 ? 2 : 1;   // 2048 threads per SM at most
+  int nsplit = sm_count() * per_sm / units;
+  if (nsplit < 1) nsplit = 1;
+  if (nsplit > V) nsplit = (int)V;
+  small_relight_kernel<LOG2N><<<units * nsplit, kSWarps * 32, SM, st>>>(T, V, faces, planes, vparams, partial, nsplit);
+  HS_CHECK_LAUNCH("small_relight_kernel");
+  return HS_OK;
+}
+
+}  // namespace
+
+size_t relight_small_planes_workspace_bytes(long long V, int faces, int log2n) {
+  return (size_t)faces * 3 * log2n * ((size_t)1 << (2 * log2n)) * 4 + (size_t)V * 3 * faces * 4 + 256;
+}
+
+// N <= 64 (log2n <= 6): every level from residue planes
+hs_status launch_relight_small_planes(const float* T, long long V, int faces, const float* light, int log2n,
+                                      const double* fields64, long long face_stride, const int4* vparams, float* R,
+                                      void* ws, cudaStream_t st) {
+  if (log2n < 1 || log2n > 6) return HS_ERR_UNSUPPORTED;
+  float* planes = reinterpret_cast<float*>(ws);
+  float* partial = planes + (size_t)faces * 3 * log2n * ((size_t)1 << (2 * log2n));
+  const int units = 3 * faces;
+  const size_t psm = (size_t)2 * ((size_t)1 << (2 * log2n)) * 8;
+  static bool attr = false;
+  if (!attr) {
+    HS_CHECK_CUDA(cudaFuncSetAttribute(small_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8),
+                  "cudaFuncSetAttribute(small_planes_kernel)");
+    attr = true;
+  }
+  small_planes_kernel<<<units, 512, psm, st>>>(fields64, face_stride, log2n, planes);
+  HS_CHECK_LAUNCH("small_planes_kernel");
+  hs_status s = HS_OK;
+  switch (log2n) {
+    case 1: s = launch_small_relight<1>(T, V, faces, planes, vparams, partial, st); break;
+    case 2: s = launch_small_relight<2>(T, V, faces, planes, vparams, partial, st); break;
+    case 3: s = launch_small_relight<3>(T, V, faces, planes, vparams, partial, st); break;
+    case 4: s = launch_small_relight<4>(T, V, faces, planes, vparams, partial, st); break;
+    case 5: s = launch_small_relight<5>(T, V, faces, planes, vparams, partial, st); break;
+    default: s = launch_small_relight<6>(T, V, faces, planes, vparams, partial, st); break;
+  }
+  if (s != HS_OK) return s;
+  small_finish_kernel<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(partial, T, light, V, faces, log2n, R);
+  HS_CHECK_LAUNCH("small_finish_kernel");
+  return HS_OK;
+}
+
+namespace {
 }  // namespace
 
 size_t relight_planes_workspace_bytes(long long V, int faces) {
