@@ -158,9 +158,9 @@ HS_API size_t relight_workspace_bytes(int faces, int k_face, int batch);
  *   vertex_shifts  DEVICE pointer [num_vertices][2] fp32 (sy, sx), finite.
  *   radiance       [num_vertices] fp32.
  *   workspace      >= relight_shifted_workspace_bytes(...) bytes.
- * Paths: N = 32, 64 fused per-vertex stencil; N = 128 residue planes of the light (exact: the box
- * shift is four integer rolls and the bottom-up commutes with even rolls);
- * larger N the chunked tile shift + row dot.  The light's fields are built in fp64.
+ * Paths: N <= 128 residue planes of the light (exact: the box shift is four integer rolls and the
+ * bottom-up commutes with even rolls, so every output level is a rolled read of planes built once
+ * per call from the light's fp64 fields); larger N the chunked tile shift + row dot.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, int faces,
                                    const float* light, int log2n, const float* vertex_shifts,
