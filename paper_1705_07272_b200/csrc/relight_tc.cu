@@ -100,6 +100,17 @@ __global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __res
   }
 }
 
+// (v - h) * 2^11 for a pair, as two packed f32x2 instructions (sm_100 FADD2 / FMUL2): the same
+// roundings as the scalar form (the difference is exact, the power-of-two scale is exact)
+__device__ __forceinline__ float2 resid2048(float2 v, float2 h) {
+  float2 r;
+  asm("{\n\t.reg .b64 va, ha, d, k;\n\tmov.b64 va, {%2, %3};\n\tmov.b64 ha, {%4, %5};\n\t"
+      "mov.b64 k, {%6, %6};\n\tsub.rn.f32x2 d, va, ha;\n\tmul.rn.f32x2 d, d, k;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(v.x), "f"(v.y), "f"(h.x), "f"(h.y), "f"(2048.f));
+  return r;
+}
+
 // ------------------------------------------------------------------------------- main kernel
 __global__ void __launch_bounds__(kThreads, 1)
     relight_tc_kernel(const __grid_constant__ CUtensorMap tmapT, const uint8_t* __restrict__ ltiles,
@@ -238,8 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const __half2 h1 = __floats2half2_rn(v.z, v.w);
             const float2 f0 = __half22float2(h0);
             const float2 f1 = __half22float2(h1);
-            const __half2 l0 = __floats2half2_rn((v.x - f0.x) * 2048.f, (v.y - f0.y) * 2048.f);
-            const __half2 l1 = __floats2half2_rn((v.z - f1.x) * 2048.f, (v.w - f1.y) * 2048.f);
+            const float2 r0 = resid2048(make_float2(v.x, v.y), f0);   // (v - hi) 2^11, exact
+            const float2 r1 = resid2048(make_float2(v.z, v.w), f1);
+            const __half2 l0 = __floats2half2_rn(r0.x, r0.y);
+            const __half2 l1 = __floats2half2_rn(r1.x, r1.y);
             hi[2 * c] = *reinterpret_cast<const uint32_t*>(&h0);
             hi[2 * c + 1] = *reinterpret_cast<const uint32_t*>(&h1);
             lo[2 * c] = *reinterpret_cast<const uint32_t*>(&l0);
