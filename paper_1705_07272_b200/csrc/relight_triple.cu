@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float a = o[32 * h + 2 * c], b = o[32 * h + 2 * c + 1];
             const __half2 hh = __floats2half2_rn(a, b);
             const float2 hf = __half22float2(hh);
-            const __half2 ll = __floats2half2_rn((a - hf.x) * 2048.f, (b - hf.y) * 2048.f);
+            const float2 rr = resid2048(make_float2(a, b), hf);   // (o - hi) 2^11, exact
+            const __half2 ll = __floats2half2_rn(rr.x, rr.y);
             hi[c] = *reinterpret_cast<const uint32_t*>(&hh);
             lo[c] = *reinterpret_cast<const uint32_t*>(&ll);
           }

@@ -124,5 +124,16 @@ inline int num_sms() {
   return n;
 }
 
+// (v - h) * 2^11 for a pair, as two packed f32x2 instructions (sm_100 FADD2 / FMUL2): the same
+// roundings as the scalar form (the difference is exact, the power-of-two scale is exact)
+__device__ __forceinline__ float2 resid2048(float2 v, float2 h) {
+  float2 r;
+  asm("{\n\t.reg .b64 va, ha, d, k;\n\tmov.b64 va, {%2, %3};\n\tmov.b64 ha, {%4, %5};\n\t"
+      "mov.b64 k, {%6, %6};\n\tsub.rn.f32x2 d, va, ha;\n\tmul.rn.f32x2 d, d, k;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(v.x), "f"(v.y), "f"(h.x), "f"(h.y), "f"(2048.f));
+  return r;
+}
+
 }  // namespace tc
 }  // namespace hs
