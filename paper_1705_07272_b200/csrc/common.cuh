@@ -106,7 +106,7 @@ __host__ __device__ inline FaceParam make_face_param_1d(double s, int n) {
   return fp;
 }
 
-constexpr int kMaxFacesPerLaunch = 512;
+constexpr int kMaxFacesPerLaunch = 1024;   // ShiftArgs stays under the 32 KB kernel-parameter limit
 
 struct ShiftArgs {
   const float* in;            // face g reads in + (g / faces) * in_batch_stride + (g % faces) * K
