@@ -81,6 +81,53 @@ __global__ void __launch_bounds__(256) relight_gemv_kernel(const float* __restri
   }
 }
 
+// Short rows (K <= 4096, one frame): one row per 256-thread block, every thread's float4 loads
+// issued at once -- a single HBM round trip per row instead of K / 512 dependent ones (the c2
+// step is latency-bound).  Fixed reduction order (thread, warp tree, warps in order): per-row
+// results depend on K only, not on the row count or the sharding.
+constexpr int kShortK = 4096;
+__global__ void __launch_bounds__(256) relight_gemv_short_kernel(const float* __restrict__ T, long long V, int K,
+                                                                 int kshift, const float* __restrict__ L,
+                                                                 long long lstride, float* __restrict__ R) {
+  __shared__ float part[8];
+  const int kmask = (1 << kshift) - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (long long row = blockIdx.x; row < V; row += gridDim.x) {
+    const float* Tr = T + row * (long long)K;
+    float4 t[kShortK / 1024], l[kShortK / 1024];
+#pragma unroll
+    for (int u = 0; u < kShortK / 1024; ++u) {
+      const int k = (tid + u * 256) * 4;
+      if (k < K) {
+        t[u] = ld_stream(Tr + k);
+        l[u] = __ldg(reinterpret_cast<const float4*>(L + (long long)(k >> kshift) * lstride + (k & kmask)));
+      } else {
+        t[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        l[u] = t[u];
+      }
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int u = 0; u < kShortK / 1024; ++u) {
+      acc = fmaf(t[u].x, l[u].x, acc);
+      acc = fmaf(t[u].y, l[u].y, acc);
+      acc = fmaf(t[u].z, l[u].z, acc);
+      acc = fmaf(t[u].w, l[u].w, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      float sum = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += part[w];
+      R[row] = sum;
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int GM = 128, GN = 64, GK = 32;
 
 __global__ void __launch_bounds__(256) relight_gemm_kernel(const float* __restrict__ T, long long V, int K,
@@ -222,6 +269,14 @@ hs_status launch_relight(const float* T, long long V, int faces, int kface, cons
   int kshift = 0;
   while ((1 << kshift) < kface) ++kshift;
   const long long lbatch = (long long)faces * lstride;
+  if (batch == 1 && K <= kShortK) {
+    long long blocks = V;
+    const long long cap = (long long)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    relight_gemv_short_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, V, K, kshift, L, lstride, R);
+    HS_CHECK_LAUNCH("relight_gemv_short_kernel");
+    return HS_OK;
+  }
   switch (batch) {
     case 1: return gemv<1>(T, V, K, kshift, L, lstride, lbatch, R, st);
     case 2: return gemv<2>(T, V, K, kshift, L, lstride, lbatch, R, st);
