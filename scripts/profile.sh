@@ -3,7 +3,7 @@
 #   1) default bench (plain)                       -> gpurun_out/bench_${TAG}.log
 #   2) launch list of a short bench under ncu     -> gpurun_out/launches_${TAG}.csv
 #   3) ncu --set full of relight_tc / shift tile  -> gpurun_out/prof_${TAG}.ncu-rep
-#   4) ncu --set full of the fused c4 unit kernel -> gpurun_out/prof_c4_${TAG}.ncu-rep
+#   4) ncu --set full of the fused c4 residue-plane kernels -> gpurun_out/prof_c4_${TAG}.ncu-rep
 set -u
 TAG=${1:-r01}
 mkdir -p gpurun_out
@@ -17,6 +17,6 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"re
     -c 2 -o gpurun_out/prof_${TAG} $CMD > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "full exit=$?" >> gpurun_out/ncu_full_${TAG}.log
 timeout 300 python scripts/run_c4.py 20000 1 > gpurun_out/c4plain_${TAG}.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:relight_shifted_unit -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"planes_(a|c)_kernel" -c 2 \
     -o gpurun_out/prof_c4_${TAG} python scripts/run_c4.py 20000 1 > gpurun_out/ncu_c4_${TAG}.log 2>&1
 echo "c4 exit=$?" >> gpurun_out/ncu_c4_${TAG}.log
