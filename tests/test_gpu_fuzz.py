@@ -29,7 +29,7 @@ def _shift_value(rng, N):
     return float(rng.uniform(-1e4, 1e4))            # large magnitude
 
 
-@pytest.mark.parametrize("case", range(40))
+@pytest.mark.parametrize("case", range(64))
 def test_shift_fuzz(case):
     import torch
     import paper_1705_07272_b200 as hs
@@ -109,7 +109,7 @@ def test_shift1d_fuzz(case):
     assert err <= 1e-5, (n, faces, batch, band, err)
 
 
-@pytest.mark.parametrize("case", range(10))
+@pytest.mark.parametrize("case", range(24))
 def test_relight_shifted_fuzz(case):
     """Per-vertex shifts (a7): random N, faces, vertex count (ragged), shift classes."""
     import torch
@@ -169,7 +169,7 @@ def test_relight_dense_fuzz(case):
     assert err <= 1e-5, (k, faces, B, V, err)
 
 
-@pytest.mark.parametrize("case", range(8))
+@pytest.mark.parametrize("case", range(16))
 def test_relight_triple_fuzz(case):
     import torch
     import paper_1705_07272_b200 as hs
