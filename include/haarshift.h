@@ -57,6 +57,7 @@ typedef enum {
 } hs_status;
 
 #define HS_MAX_LOG2N 12
+#define HS_MAX_FACES 1024   /* faces per batch entry of the shift entry points (one launch's parameter block) */
 
 /* ---------------------------------------------------------------------------------------------
  * haar_shift_coeffs -- shift of Haar coefficient pyramids computed directly in the Haar domain
@@ -75,7 +76,7 @@ typedef enum {
  *                 HAAR1 prefix holding the scaling coefficient and levels < band_levels.
  *   ndim          1 or 2.
  *   log2n         1 .. HS_MAX_LOG2N (N = 2^log2n).
- *   faces, batch  >= 1.
+ *   faces         1 .. HS_MAX_FACES;  batch >= 1 (any count: launches are chunked by batch entry).
  *   shifts_host   HOST pointer, [batch][faces][ndim] fp64, (sy, sx) order in 2D, any finite real
  *                 value (reduced mod N internally in fp64).
  *   band_levels   0 .. log2n (log2n = full pyramid).
@@ -130,15 +131,23 @@ HS_API size_t haar_shift_coarse_workspace_bytes(int in_log2n, int start_level, i
  *                 can be passed.  light_face_stride >= k_face and a multiple of 4.
  *   k_face        a power of 4 (the HAAR1 prefix 4^k: scaling + levels < k), >= 4.
  *   batch         1 .. 1024 light/rotation frames.
- *   radiance      [num_vertices][batch] fp32.
+ *   radiance      [num_vertices][batch] fp32, must not overlap transfer, light or workspace
+ *                 (HS_ERR_INVALID_ARG); 16-byte aligned when the tensor-core path runs (workspace
+ *                 size > 0), 4-byte aligned otherwise (HS_ERR_ALIGNMENT).
  *   workspace     device scratch of >= relight_workspace_bytes(faces, k_face, batch) bytes,
  *                 1024-byte aligned (may be NULL when that size is 0).
  * Accumulation is fp32.  batch <= 8: CUDA-core streaming GEMV.  batch a multiple of 64 with
- * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16 (T and the
- * per-frame-scaled light each split into fp16 hi + lo, three products, fp32 accumulation in TMEM
- * drained into fp32 registers every 1024 k; ~2^-21 relative per product; requires |T| < 2^15 --
- * transfer coefficients of an orthonormal basis are bounded by the function's L2 norm).  Other
- * batches: CUDA-core tiled GEMM.
+ * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16.  Every 64-k
+ * block of every transfer row is scaled by its own power of two 2^e (max |T| of the block ->
+ * [2^14, 2^15)) and every light frame by its own power of two s_b before the fp16 hi + lo split;
+ * three products per block accumulate in fp32 in TMEM, the epilogue drains each block into fp32
+ * registers with the factor 2^-e and divides by s_b at the end.  Contract: ~2^-21 relative per
+ * product for any finite fp32 transfer and light values (a block whose max |T| is below 2^-112,
+ * i.e. outside fp32's normal range after the 2^-14 headroom, loses relative precision
+ * gracefully); the result overflows only if sum |T L| * s_b / max|L_b s_b| does, i.e. when
+ * |T| > ~2^100 together with K * 2^15 headroom.  Tested at T scaled by 2^-30 ... 2^60 and
+ * with mixed row / block magnitudes (tests/test_gpu_range.py).  Other batches: CUDA-core tiled
+ * GEMM (fp32 FMA).
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
                            const float* light, int64_t light_face_stride, int batch,
@@ -154,9 +163,10 @@ HS_API size_t relight_workspace_bytes(int faces, int k_face, int batch);
  *           P:514 (coarser levels by the recursive h_s / h_t filters).
  *
  *   transfer       [num_vertices][faces*N*N] fp32 (full pyramids per face, 64-bit indexing).
+ *   faces          1 .. HS_MAX_FACES.
  *   light          [faces][N*N] fp32, one pyramid per face.
  *   vertex_shifts  DEVICE pointer [num_vertices][2] fp32 (sy, sx), finite.
- *   radiance       [num_vertices] fp32.
+ *   radiance       [num_vertices] fp32, must not overlap transfer, light or vertex_shifts.
  *   workspace      >= relight_shifted_workspace_bytes(...) bytes.
  * Paths: N <= 128 residue planes of the light (exact: the box shift is four integer rolls and the
  * bottom-up commutes with even rolls, so every output level is a rolled read of planes built once
@@ -180,7 +190,8 @@ HS_API size_t relight_shifted_workspace_bytes(int64_t num_vertices, int faces, i
  *   indices       DEVICE [num_vertices][k_sparse] int32 in [0, total_coeffs) (duplicates add).
  *   values        DEVICE [num_vertices][k_sparse] fp32.
  *   light         DEVICE [batch][total_coeffs] fp32 (e.g. full shifted pyramids, faces concatenated).
- *   radiance      DEVICE [num_vertices][batch] fp32.
+ *   radiance      DEVICE [num_vertices][batch] fp32, no overlap with the inputs or workspace;
+ *                 8-byte aligned when batch >= 64 (float2 stores), 4-byte otherwise.
  *   workspace     >= relight_sparse_workspace_bytes(total_coeffs, batch): the light transposed to
  *                 coefficient-major [total_coeffs][batch] (one contiguous row per gathered index).
  * ------------------------------------------------------------------------------------------- */
@@ -212,12 +223,15 @@ HS_API hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_
  *                  (haar_pack_qtree below).
  *   light          DEVICE [batch][faces][light_face_stride] fp32 in HAAR1 order (the first k_face
  *                  entries of each face are used -- e.g. the band written by haar_shift_coeffs).
- *   radiance       DEVICE [num_vertices][batch] fp32.
+ *   radiance       DEVICE [num_vertices][batch] fp32, no overlap with the inputs or workspace;
+ *                  16-byte aligned on the tensor-core path (batch % 64 == 0), 4-byte otherwise.
  *   k_face         4^k with 3 <= k <= 12.
  *   workspace      >= relight_triple_workspace_bytes(...), 1024-byte aligned (HS_ERR_ALIGNMENT).
  *   Precision: fp32 inputs; the tripling terms are formed in fp32 and multiplied on the tensor
  *   cores in split fp16 (hi + 2^-11 lo) with fp32 accumulation when batch % 64 == 0 (DESIGN.md
- *   §5.8), otherwise on CUDA cores in fp32.
+ *   §5.8), each 64-term chunk of each row scaled by its own power of two first (as in
+ *   relight_vertices: any fp32 magnitude of BRDF and visibility whose tripling terms stay
+ *   finite), otherwise on CUDA cores in fp32.
  *
  * haar_pack_qtree -- HAAR1 -> qtree layout (the storage format of brdf_q / vis_q):
  *   in   DEVICE [rows][faces][in_face_stride] fp32, HAAR1 prefix of 4^log2k used per face;

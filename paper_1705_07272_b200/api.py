@@ -28,6 +28,24 @@ def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+def _log2n_pow4(K: int, what: str) -> int:
+    """log2 N of a face of K = 4**log2n coefficients; ValueError otherwise."""
+    n = int(K).bit_length() - 1
+    if K < 4 or n % 2 or (1 << n) != K:
+        raise ValueError(f"{what} must hold 4**log2n coefficients (got {K})")
+    return n // 2
+
+
+def _out(out: Optional[torch.Tensor], shape, device, name: str = "out") -> torch.Tensor:
+    """a new float32 result tensor, or the caller's `out` checked like every other device argument"""
+    if out is None:
+        return torch.empty(tuple(shape), dtype=torch.float32, device=device)
+    _dev_f32(out, name)
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(out.shape)}")
+    return out
+
+
 def enable_peer_access(peer_device: int) -> None:
     """Allow kernels on the current device to access `peer_device`'s memory (include/haarshift.h)."""
     check("hs_enable_peer_access", load().hs_enable_peer_access(int(peer_device)))
@@ -57,21 +75,16 @@ def haar_shift_coeffs(coeffs: torch.Tensor, shifts, ndim: int = 2, band_levels: 
     if coeffs.dim() != 3:
         raise ValueError("coeffs must be [batch][faces][K]")
     B, F, K = coeffs.shape
-    n = int(K).bit_length() - 1
     if ndim == 2:
-        if n % 2 or (1 << n) != K:
-            raise ValueError("2D faces must hold 4**log2n coefficients")
-        log2n = n // 2
+        log2n = _log2n_pow4(K, "2D faces")
     else:
-        if (1 << n) != K:
+        log2n = int(K).bit_length() - 1
+        if (1 << log2n) != K:
             raise ValueError("1D signals must hold 2**log2n coefficients")
-        log2n = n
     band = log2n if band_levels is None else int(band_levels)
     kb = (4 if ndim == 2 else 2) ** band
     sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(B, F, ndim))
-    if out is None:
-        out = torch.empty((B, F, kb), dtype=torch.float32, device=coeffs.device)
-    _dev_f32(out, "out")
+    out = _out(out, (B, F, kb), coeffs.device)
     need = haar_shift_workspace_bytes(ndim, log2n, F, B)
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
@@ -93,13 +106,13 @@ def haar_shift_coeffs_coarse(coeffs: torch.Tensor, shifts, start_level: int, ban
     [batch][faces][4**band] (band <= L, default L).  shifts: host [batch][faces][2] in pixels."""
     lib = load()
     _dev_f32(coeffs, "coeffs")
+    if coeffs.dim() != 3:
+        raise ValueError("coeffs must be [batch][faces][K]")
     B, F, K = coeffs.shape
-    n = (int(K).bit_length() - 1) // 2
+    n = _log2n_pow4(K, "2D faces")
     band = start_level if band_levels is None else int(band_levels)
     sh = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(B, F, 2))
-    if out is None:
-        out = torch.empty((B, F, 4 ** band), dtype=torch.float32, device=coeffs.device)
-    _dev_f32(out, "out")
+    out = _out(out, (B, F, 4 ** band), coeffs.device)
     need = haar_shift_coarse_workspace_bytes(n, start_level, F, B)
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
@@ -123,13 +136,9 @@ def haar_rotate_coeffs(coeffs: torch.Tensor, angles, out: Optional[torch.Tensor]
     _dev_f32(coeffs, "coeffs")
     B = coeffs.shape[0]
     K = coeffs.numel() // B
-    n = (int(K).bit_length() - 1) // 2
-    if 4 ** n != K:
-        raise ValueError("maps must hold 4**log2n coefficients")
+    n = _log2n_pow4(K, "maps")
     ang = np.ascontiguousarray(np.asarray(angles, dtype=np.float64).reshape(B, 2))
-    if out is None:
-        out = torch.empty_like(coeffs)
-    _dev_f32(out, "out")
+    out = _out(out, coeffs.shape, coeffs.device)
     need = haar_rotate_workspace_bytes(n, B)
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=coeffs.device)
@@ -156,9 +165,7 @@ def relight_vertices(transfer: torch.Tensor, light: torch.Tensor, faces: int, k_
     if light.dim() != 3 or light.shape[1] != faces:
         raise ValueError("light must be [batch][faces][stride]")
     B, _, stride = light.shape
-    if out is None:
-        out = torch.empty((V, B), dtype=torch.float32, device=transfer.device)
-    _dev_f32(out, "out")
+    out = _out(out, (V, B), transfer.device)
     need = relight_workspace_bytes(faces, k_face, B)
     ws_ptr = None
     if need:
@@ -182,13 +189,14 @@ def relight_vertices_shifted(transfer: torch.Tensor, light: torch.Tensor, vertex
     _dev_f32(transfer, "transfer")
     _dev_f32(light, "light")
     _dev_f32(vertex_shifts, "vertex_shifts")
+    if light.dim() != 2:
+        raise ValueError("light must be [faces][N*N]")
     F, K = light.shape
-    n = (int(K).bit_length() - 1) // 2
+    n = _log2n_pow4(K, "light faces")
     V = transfer.shape[0]
-    if transfer.numel() != V * F * K or vertex_shifts.shape != (V, 2):
-        raise ValueError("shape mismatch")
-    if out is None:
-        out = torch.empty((V,), dtype=torch.float32, device=transfer.device)
+    if transfer.numel() != V * F * K or tuple(vertex_shifts.shape) != (V, 2):
+        raise ValueError("transfer must be [V][faces*N*N] and vertex_shifts [V][2]")
+    out = _out(out, (V,), transfer.device)
     need = relight_shifted_workspace_bytes(V, F, n)
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=transfer.device)
@@ -211,11 +219,12 @@ def relight_vertices_sparse(indices: torch.Tensor, values: torch.Tensor, light: 
         raise TypeError("indices must be a contiguous CUDA int32 tensor")
     _dev_f32(values, "values")
     _dev_f32(light, "light")
+    if indices.dim() != 2 or tuple(values.shape) != tuple(indices.shape):
+        raise ValueError("indices and values must both be [V][K_s]")
     V, ks = indices.shape
     B = light.shape[0]
     C = light.numel() // B
-    if out is None:
-        out = torch.empty((V, B), dtype=torch.float32, device=values.device)
+    out = _out(out, (V, B), values.device)
     need = relight_sparse_workspace_bytes(C, B)
     if workspace is None or workspace.numel() * workspace.element_size() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=values.device)
@@ -242,9 +251,7 @@ def haar_pack_qtree(coeffs: torch.Tensor, log2k: int, out: Optional[torch.Tensor
         raise ValueError("coeffs must be [rows][faces][stride]")
     rows, F, stride = coeffs.shape
     kf = 4 ** log2k
-    if out is None:
-        out = torch.empty((rows, F * kf), dtype=torch.float32, device=coeffs.device)
-    _dev_f32(out, "out")
+    out = _out(out, (rows, F * kf), coeffs.device)
     st = lib.haar_pack_qtree(coeffs.data_ptr(), rows, F, stride, log2k, out.data_ptr(), _stream_ptr(stream))
     check("haar_pack_qtree", st)
     return out
@@ -269,9 +276,7 @@ def relight_vertices_triple(brdf_q: torch.Tensor, vis_q: torch.Tensor, light: to
     if light.dim() != 3 or light.shape[1] != faces:
         raise ValueError("light must be [batch][faces][stride]")
     B, _, stride = light.shape
-    if out is None:
-        out = torch.empty((V, B), dtype=torch.float32, device=brdf_q.device)
-    _dev_f32(out, "out")
+    out = _out(out, (V, B), brdf_q.device)
     need = relight_triple_workspace_bytes(V, faces, k_face, B)
     workspace = _aligned_workspace(need, workspace, brdf_q.device)
     st = lib.relight_vertices_triple(brdf_q.data_ptr(), vis_q.data_ptr(), V, faces, k_face, light.data_ptr(), stride,

@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -29,12 +31,43 @@ inline bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   const char* pb = (const char*)b;
   return pa < pb + nb && pb < pa + na;
 }
+inline bool aligned_to(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+// bytes spanned by `rows` rows of `row_len` floats at a row stride of `stride` floats
+inline size_t span_bytes(long long rows, long long stride, long long row_len) {
+  return (size_t)((rows - 1) * stride + row_len) * sizeof(float);
+}
 constexpr long long kRelightChunk = 128;  // vertices per chunk of the per-vertex shift path
 
 }  // namespace
 
 void set_cuda_error(cudaError_t e, const char* where) {
   snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+cudaError_t ensure_max_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, const void*, int>> done;   // (device, kernel, bytes) already set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (std::get<0>(d) == dev && std::get<1>(d) == kernel && std::get<2>(d) >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(dev, kernel, bytes);
+  return e;
 }
 
 hs_status check_device() {
@@ -98,7 +131,7 @@ hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, in
   g_launches = 0;
   if (!in || !out || !shifts_host) return HS_ERR_INVALID_ARG;
   if (ndim != 1 && ndim != 2) return HS_ERR_INVALID_ARG;
-  if (log2n < 1 || log2n > HS_MAX_LOG2N || faces < 1 || batch < 1) return HS_ERR_INVALID_ARG;
+  if (log2n < 1 || log2n > HS_MAX_LOG2N || faces < 1 || faces > HS_MAX_FACES || batch < 1) return HS_ERR_INVALID_ARG;
   if (band_levels < 0 || band_levels > log2n) return HS_ERR_INVALID_ARG;
   const long long nfaces = (long long)faces * batch;
   for (long long i = 0; i < nfaces * ndim; ++i)
@@ -129,7 +162,8 @@ hs_status haar_shift_coeffs_coarse(const float* in, float* out, int in_log2n, in
   g_launches = 0;
   if (!in || !out || !shifts_host) return HS_ERR_INVALID_ARG;
   if (in_log2n < 1 || in_log2n > HS_MAX_LOG2N || start_level < 1 || start_level > in_log2n) return HS_ERR_INVALID_ARG;
-  if (faces < 1 || batch < 1 || band_levels < 0 || band_levels > start_level) return HS_ERR_INVALID_ARG;
+  if (faces < 1 || faces > HS_MAX_FACES || batch < 1 || band_levels < 0 || band_levels > start_level)
+    return HS_ERR_INVALID_ARG;
   const long long nfaces = (long long)faces * batch;
   for (long long i = 0; i < nfaces * 2; ++i)
     if (!std::isfinite(shifts_host[i])) return HS_ERR_INVALID_ARG;
@@ -168,7 +202,16 @@ hs_status relight_vertices(const float* transfer, int64_t num_vertices, int face
   if ((long long)faces * k_face > (1ll << 30)) return HS_ERR_INVALID_ARG;
   const size_t need = relight_tc_workspace_bytes(faces, k_face, batch);
   if (need > 0 && (!workspace || workspace_bytes < need)) return HS_ERR_INVALID_ARG;
-  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance) ||
+  {
+    const long long K = (long long)faces * k_face;
+    const size_t rb = (size_t)num_vertices * batch * sizeof(float);
+    if (overlap(radiance, rb, transfer, (size_t)num_vertices * K * 4) ||
+        overlap(radiance, rb, light, span_bytes((long long)batch * faces, light_face_stride, k_face)) ||
+        (need > 0 && overlap(radiance, rb, workspace, need)))
+      return HS_ERR_INVALID_ARG;
+  }
+  // the tensor-core epilogue stores float4 rows; the CUDA-core paths store single floats
+  if (!aligned16(transfer) || !aligned16(light) || !aligned_to(radiance, need > 0 ? 16 : 4) ||
       (need > 0 && (reinterpret_cast<uintptr_t>(workspace) & 1023)))
     return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
@@ -196,10 +239,18 @@ hs_status relight_vertices_shifted(const float* transfer, int64_t num_vertices, 
   g_last_launches = 0;
   g_launches = 0;
   if (!transfer || !light || !vertex_shifts || !radiance || !workspace) return HS_ERR_INVALID_ARG;
-  if (num_vertices < 1 || faces < 1 || log2n < 1 || log2n > HS_MAX_LOG2N) return HS_ERR_INVALID_ARG;
+  if (num_vertices < 1 || faces < 1 || faces > HS_MAX_FACES || log2n < 1 || log2n > HS_MAX_LOG2N)
+    return HS_ERR_INVALID_ARG;
+  {
+    const long long K = (long long)faces << (2 * log2n);
+    const size_t rb = (size_t)num_vertices * sizeof(float);
+    if (overlap(radiance, rb, transfer, (size_t)num_vertices * K * 4) || overlap(radiance, rb, light, (size_t)K * 4) ||
+        overlap(radiance, rb, vertex_shifts, (size_t)num_vertices * 8))
+      return HS_ERR_INVALID_ARG;
+  }
   const size_t need = relight_shifted_workspace_bytes(num_vertices, faces, log2n);
   if (workspace_bytes < need) return HS_ERR_INVALID_ARG;
-  if (!aligned16(transfer) || !aligned16(light) || !aligned16(radiance) || !aligned16(workspace) ||
+  if (!aligned16(transfer) || !aligned16(light) || !aligned_to(radiance, 4) || !aligned16(workspace) ||
       (reinterpret_cast<uintptr_t>(vertex_shifts) & 7))
     return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
@@ -244,7 +295,16 @@ hs_status relight_vertices_sparse(const int32_t* indices, const float* values, i
   if (num_vertices < 1 || k_sparse < 1 || total_coeffs < 1 || total_coeffs >= (1ll << 31)) return HS_ERR_INVALID_ARG;
   if (batch < 1 || batch > 1024) return HS_ERR_INVALID_ARG;
   if (workspace_bytes < relight_sparse_workspace_bytes(total_coeffs, batch)) return HS_ERR_INVALID_ARG;
-  if (!aligned16(indices) || !aligned16(values) || !aligned16(light) || !aligned16(radiance) || !aligned16(workspace))
+  {
+    const size_t rb = (size_t)num_vertices * batch * sizeof(float);
+    const size_t pb = (size_t)num_vertices * k_sparse * 4;
+    if (overlap(radiance, rb, indices, pb) || overlap(radiance, rb, values, pb) ||
+        overlap(radiance, rb, light, (size_t)batch * total_coeffs * 4) || overlap(radiance, rb, workspace, workspace_bytes))
+      return HS_ERR_INVALID_ARG;
+  }
+  // the 64-frame kernel stores float2 pairs; the scalar kernel single floats
+  if (!aligned16(indices) || !aligned16(values) || !aligned16(light) || !aligned_to(radiance, batch >= 64 ? 8 : 4) ||
+      !aligned16(workspace))
     return HS_ERR_ALIGNMENT;
   hs_status s = check_device();
   if (s != HS_OK) return s;
@@ -345,7 +405,16 @@ hs_status relight_vertices_triple(const float* brdf_q, const float* vis_q, int64
   if (light_face_stride < k_face || (light_face_stride & 3)) return HS_ERR_INVALID_ARG;
   if ((long long)faces * k_face > (1ll << 30)) return HS_ERR_INVALID_ARG;
   if (workspace_bytes < relight_triple_workspace_bytes_impl(num_vertices, faces, k_face, batch)) return HS_ERR_INVALID_ARG;
-  if (!aligned16(brdf_q) || !aligned16(vis_q) || !aligned16(light) || !aligned16(radiance) ||
+  {
+    const size_t rb = (size_t)num_vertices * batch * sizeof(float);
+    const size_t qb = (size_t)num_vertices * faces * k_face * 4;
+    if (overlap(radiance, rb, brdf_q, qb) || overlap(radiance, rb, vis_q, qb) ||
+        overlap(radiance, rb, light, span_bytes((long long)batch * faces, light_face_stride, k_face)) ||
+        overlap(radiance, rb, workspace, workspace_bytes))
+      return HS_ERR_INVALID_ARG;
+  }
+  if (!aligned16(brdf_q) || !aligned16(vis_q) || !aligned16(light) ||
+      !aligned_to(radiance, relight_tc_eligible(faces, k_face, batch) ? 16 : 4) ||
       (reinterpret_cast<uintptr_t>(workspace) & 1023))
     return HS_ERR_ALIGNMENT;
   hs_status s = check_device();

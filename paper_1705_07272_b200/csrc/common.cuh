@@ -17,6 +17,13 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 extern thread_local int g_launches;       // kernel launches enqueued by the current ABI call
 
+// Per-device state (a process may drive several GPUs): the SM count of the current device, and
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applied once per (device, kernel).
+int device_sm_count();
+cudaError_t ensure_max_smem(const void* kernel, int bytes);
+#define HS_SMEM_ATTR(kernel, bytes) \
+  HS_CHECK_CUDA(::hs::ensure_max_smem(reinterpret_cast<const void*>(kernel), (int)(bytes)), "cudaFuncSetAttribute(" #kernel ")")
+
 #define HS_CHECK_LAUNCH(where)                                   \
   do {                                                           \
     cudaError_t e_ = cudaGetLastError();                         \

@@ -223,17 +223,7 @@ __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ T
   }
 }
 
-int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
-  }
-  return cached;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int B, int RPW>
 hs_status gemv_launch(const float* T, long long V, int K, int kshift, const float* L, long long lstride,

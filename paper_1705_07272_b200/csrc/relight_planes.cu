@@ -336,16 +336,7 @@ __global__ void planes_finish_kernel(const float* __restrict__ partial, const fl
   R[v] = s;
 }
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return device_sm_count(); }
 
 // ------------------------------------------------------------------------------- N <= 64: every level
 // For small faces every level's residue planes fit in shared memory at once (n levels x 4^n
@@ -472,12 +463,7 @@ template <int LOG2N>
 hs_status launch_small_relight(const float* T, long long V, int faces, const float* planes, const int4* vparams,
                                float* partial, cudaStream_t st) {
   constexpr int SM = LOG2N * (1 << (2 * LOG2N)) * 4;
-  static bool attr = false;
-  if (!attr) {
-    HS_CHECK_CUDA(cudaFuncSetAttribute(small_relight_kernel<LOG2N>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM),
-                  "cudaFuncSetAttribute(small_relight_kernel)");
-    attr = true;
-  }
+  HS_SMEM_ATTR(small_relight_kernel<LOG2N>, SM);
   const int units = 3 * faces;
   const int per_sm = (227 * 1024) / (SM + 1024) >= 2 ? 2 : 1;   // 2048 threads per SM at most
   int nsplit = sm_count() * per_sm / units;
@@ -503,12 +489,7 @@ hs_status launch_relight_small_planes(const float* T, long long V, int faces, co
   float* partial = planes + (size_t)faces * 3 * log2n * ((size_t)1 << (2 * log2n));
   const int units = 3 * faces;
   const size_t psm = (size_t)2 * ((size_t)1 << (2 * log2n)) * 8;
-  static bool attr = false;
-  if (!attr) {
-    HS_CHECK_CUDA(cudaFuncSetAttribute(small_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8),
-                  "cudaFuncSetAttribute(small_planes_kernel)");
-    attr = true;
-  }
+  HS_SMEM_ATTR(small_planes_kernel, 2 * 4096 * 8);
   small_planes_kernel<<<units, 512, psm, st>>>(fields64, face_stride, log2n, planes);
   HS_CHECK_LAUNCH("small_planes_kernel");
   hs_status s = HS_OK;
@@ -539,16 +520,9 @@ hs_status launch_relight_planes(const float* T, long long V, int faces, const fl
   float* planes = reinterpret_cast<float*>(ws);
   float* partial = planes + (size_t)faces * 3 * kPlanesPerUnit;
   const int units = 3 * faces;
-  static bool attr = false;
-  if (!attr) {
-    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4096 * 8),
-                  "cudaFuncSetAttribute(planes_kernel)");
-    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem),
-                  "cudaFuncSetAttribute(planes_a_kernel)");
-    HS_CHECK_CUDA(cudaFuncSetAttribute(planes_c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem),
-                  "cudaFuncSetAttribute(planes_c_kernel)");
-    attr = true;
-  }
+  HS_SMEM_ATTR(planes_kernel, 4 * 4096 * 8);
+  HS_SMEM_ATTR(planes_a_kernel, kASmem);
+  HS_SMEM_ATTR(planes_c_kernel, kCSmem);
   planes_kernel<<<units, 512, 4 * 4096 * 8, st>>>(fields64, face_stride, planes);
   HS_CHECK_LAUNCH("planes_kernel");
   planes3_kernel<<<units, 256, 0, st>>>(planes);

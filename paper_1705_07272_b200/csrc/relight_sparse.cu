@@ -140,16 +140,7 @@ __global__ void __launch_bounds__(256) relight_sparse64_kernel(const int* __rest
   }
 }
 
-int sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sms() { return device_sm_count(); }
 
 }  // namespace
 

@@ -1,25 +1,27 @@
 // Relight on the 5th-generation tensor cores (batch % 64 == 0):
 //   R[v][b] = sum_k T[v][k] L[b][k]        (double product, PAPER.md eq:tripleSum P:253-266)
-// in split-precision fp16 with fp32 accumulation in TMEM, accurate to ~2^-21 relative per
-// product:
-//   T = T_hi + 2^-11 T_lo,  L_b s_b = L_hi + 2^-11 L_lo   (fp16 pieces, s_b a per-frame power of 2)
-//   acc_hh = sum T_hi L_hi,  acc_x = sum (T_hi L_lo + T_lo L_hi),
-//   R = (acc_hh + 2^-11 acc_x) / s_b          (the dropped T_lo L_lo term is ~2^-22)
+// in split-precision fp16 with fp32 accumulation in TMEM.  Per 64-k block kb of
+// row v, with e_vk a power-of-two exponent chosen from the block's own max |T| and s_b a per-frame
+// power of two chosen from max |L_b|:
+//   T 2^e = T_hi + 2^-11 T_lo,  L_b s_b = L_hi + 2^-11 L_lo   (fp16 pieces, max |.| in [2^14, 2^15))
+//   acc_hh = sum_kb T_hi L_hi,  acc_x = sum_kb (T_hi L_lo + T_lo L_hi)
+//   R = sum_kb 2^-e (acc_hh + 2^-11 acc_x) / s_b     (the dropped T_lo L_lo term is ~2^-22)
+// so the split is relative to each block's magnitude for any fp32 T (no fp16 overflow or
+// subnormal loss), and the tensor-core accumulation chain is one 64-k block long.
 //
 // Kernel anatomy (one CTA per SM, persistent over 128-row tiles, 12 warps):
 //   warp 0      TMA producer: T tile [128 rows x 64 k] fp32 (two 128B-swizzled boxes) + the
 //               pre-swizzled [L_hi | L_lo] band tile [128 x 64] fp16 (one bulk copy) per stage;
 //   warp 1      MMA issuer (one thread): per 16-k step, tcgen05.mma kind::f16 with A from TMEM:
 //                 D[acc_hh | acc_x] (N=128) += T_hi x [L_hi | L_lo];  D[acc_x] (N=64) += T_lo x L_hi
+//               into accumulator buffer (block count & 1), committed to the epilogue per block;
 //   warp 2      TMEM allocator (512 columns: 4 A stages x 64 + 2 accumulator buffers x 128);
-//   warps 4-7   converters: read their row of the T tile from smem, split fp32 -> fp16 hi/lo and
-//               tcgen05.st them into the A stage (lane = row) -- T never round-trips through HBM;
-//   warps 8-11  epilogue: every KG = 16 k-blocks the MMA switches accumulator buffer and the
-//               epilogue drains the finished one (tcgen05.ld both accumulators, combine) into
-//               fp32 registers, then scales and stores the R rows at the end of the tile.  The
-//               tensor-core accumulation loses precision linearly in the chain length (3.1e-5 at
-//               K = 24576 as one chain, 2.0e-6 drained every 1024 k); the two buffers keep the
-//               drains off the MMA's critical path.
+//   warps 4-7   converters: read their row of the T tile from smem, pick e_vk from the row's 64
+//               values, split T 2^e -> fp16 hi/lo and tcgen05.st them into the A stage (lane = row)
+//               -- T never round-trips through HBM; e_vk goes to the epilogue through an int8 ring;
+//   warps 8-11  epilogue: per k block, tcgen05.ld both accumulators of the finished buffer and add
+//               2^-e (acc_hh + 2^-11 acc_x) into fp32 registers; at the end of the tile scale by
+//               1/s_b and store the R rows.  The two buffers keep the drains off the MMA's path.
 // All hand-offs are mbarriers; tcgen05.commit signals MMA completion.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -40,14 +42,11 @@ constexpr int BK = 64;            // k per stage
 constexpr int BN = 64;            // frames per block (MMA N of each accumulator)
 constexpr int STAGES = 4;         // smem stages
 constexpr int ASTAGES = 4;        // TMEM A stages
-#ifndef HS_TC_KG
-#define HS_TC_KG 16
-#endif
-constexpr int KG = HS_TC_KG;      // k-blocks per accumulation group, drained by the epilogue into fp32 registers
 constexpr int T_STAGE = BM * BK * 4;         // 32 KB
 constexpr int L_STAGE = 2 * BN * BK * 2;     // 16 KB: [L_hi 64 rows | L_lo 64 rows] x 128 B
 constexpr int SMEM_TILES = STAGES * (T_STAGE + L_STAGE);
-constexpr int SMEM_BYTES = SMEM_TILES + 1024 /*align*/ + 256 /*barriers*/ + BN * 4 + 64;
+constexpr int EXP_OFF = SMEM_TILES + 256;    // int8 exponent ring [kExpRing][BM] after the barriers
+constexpr int SMEM_BYTES = EXP_OFF + kExpRing * BM + 1024 /*align*/;
 constexpr int kThreads = 384;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t ACC_COL0 = ASTAGES * 64;  // 256
@@ -116,7 +115,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* aempty = bars + 2 * STAGES + ASTAGES;      // [ASTAGES]  MMA commit -> converters
   uint64_t* tfull = bars + 2 * STAGES + 2 * ASTAGES;   // [2]        MMA commit -> epilogue
   uint64_t* tempty = tfull + 2;                        // [2]        epilogue (128) -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* efull = tempty + 2;                        // [kExpRing]  converters (128) -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(efull + kExpRing);
+  int8_t* sexp = reinterpret_cast<int8_t*>(smem + EXP_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = K / BK;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 128);
     }
+    for (int s = 0; s < kExpRing; ++s) mbar_init(&efull[s], 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -175,16 +177,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0, astage = 0;
       uint32_t phase = 0, aphase = 0;
-      int gi = 0;   // accumulation group (KG k-blocks) counter: buffer gi & 1
+      int gi = 0;   // k-block counter: accumulator buffer gi & 1
       const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
       for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb, ++gi) {
           const int acc = gi & 1;
-          const bool first = (kb % KG) == 0;
-          if (first) {
-            mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
-            fence_after();
-          }
+          mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
           const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
           mbar_wait(&full[stage], phase);
           mbar_wait(&afull[astage], aphase);
@@ -194,11 +192,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bd = sw128_desc(lbase + kk * 32);
             const uint32_t ahi = tmem + astage * 64 + kk * 8;
-            tc_mma_ts(dhh, ahi, bd, id128, (!first || kk) ? 1u : 0u);   // [acc_hh | acc_x] += T_hi x [L_hi | L_lo]
-            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);                  // acc_x += T_lo x L_hi
+            tc_mma_ts(dhh, ahi, bd, id128, kk ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) T_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);     // acc_x += T_lo x L_hi
           }
           tc_commit(&empty[stage]);
           tc_commit(&aempty[astage]);
+          tc_commit(&tfull[acc]);   // block complete: the epilogue drains it into registers
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -206,10 +205,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++astage == ASTAGES) {
             astage = 0;
             aphase ^= 1;
-          }
-          if ((kb % KG) == KG - 1 || kb == nkb - 1) {
-            tc_commit(&tfull[acc]);   // group complete: the epilogue drains it into registers
-            ++gi;
           }
         }
       }
@@ -221,31 +216,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     int stage = 0, astage = 0;
     uint32_t phase = 0, aphase = 0;
+    int gi = 0;
     for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb, ++gi) {
         mbar_wait(&full[stage], phase);
         mbar_wait(&aempty[astage], aphase ^ 1);
         fence_after();
-        const uint8_t* tb = sT + stage * T_STAGE;
+        const uint8_t* tb = sT + stage * T_STAGE + row * 128;
+        float4 v[16];
+        float mx = 0.f;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          v[c] = *reinterpret_cast<const float4*>(tb + (c >> 3) * (T_STAGE / 2) + (((c & 7) ^ (row & 7)) << 4));
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w))));
+        }
+        const int e = split_exponent(mx);
+        const float sc = pow2i(e);
+        const int slot = gi & (kExpRing - 1);
+        sexp[slot * BM + row] = (int8_t)e;
+        mbar_arrive(&efull[slot]);
 #pragma unroll
         for (int box = 0; box < 2; ++box) {
           uint32_t hi[16], lo[16];
-          const uint8_t* rowp = tb + box * (T_STAGE / 2) + row * 128;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
-            const __half2 h0 = __floats2half2_rn(v.x, v.y);
-            const __half2 h1 = __floats2half2_rn(v.z, v.w);
-            const float2 f0 = __half22float2(h0);
-            const float2 f1 = __half22float2(h1);
-            const float2 r0 = resid2048(make_float2(v.x, v.y), f0);   // (v - hi) 2^11, exact
-            const float2 r1 = resid2048(make_float2(v.z, v.w), f1);
-            const __half2 l0 = __floats2half2_rn(r0.x, r0.y);
-            const __half2 l1 = __floats2half2_rn(r1.x, r1.y);
-            hi[2 * c] = *reinterpret_cast<const uint32_t*>(&h0);
-            hi[2 * c + 1] = *reinterpret_cast<const uint32_t*>(&h1);
-            lo[2 * c] = *reinterpret_cast<const uint32_t*>(&l0);
-            lo[2 * c + 1] = *reinterpret_cast<const uint32_t*>(&l1);
+            const float4 x = v[box * 8 + c];
+            split_pair(x.x, x.y, sc, hi[2 * c], lo[2 * c]);
+            split_pair(x.z, x.w, sc, hi[2 * c + 1], lo[2 * c + 1]);
           }
           tmem_st16(lane_base + astage * 64 + box * 16, hi);
           tmem_st16(lane_base + astage * 64 + 32 + box * 16, lo);
@@ -276,7 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-      for (int g0 = 0; g0 < nkb; g0 += KG, ++gi) {
+      for (int kb = 0; kb < nkb; ++kb, ++gi) {
+        const int slot = gi & (kExpRing - 1);
+        mbar_wait(&efull[slot], (gi / kExpRing) & 1);
+        const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row's block
         const int acc = gi & 1;
         mbar_wait(&tfull[acc], (gi >> 1) & 1);
         fence_after();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += fmaf(xx[j], 1.f / 2048.f, hh[j]);
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] = fmaf(fmaf(xx[j], 1.f / 2048.f, hh[j]), rs, sum[c * 16 + j]);
         }
         fence_before();
         mbar_arrive(&tempty[acc]);
@@ -365,12 +365,7 @@ hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, c
     set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(T)");
     return HS_ERR_CUDA;
   }
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(relight_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  });
-  HS_CHECK_CUDA(attr_err, "cudaFuncSetAttribute(relight_tc_kernel)");
+  HS_SMEM_ATTR(relight_tc_kernel, SMEM_BYTES);
 
   relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv);
   HS_CHECK_LAUNCH("relight_tc_prep_kernel");

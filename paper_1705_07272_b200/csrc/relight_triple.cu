@@ -30,10 +30,11 @@
 //     warp 3  bulk-copy producer of the pre-split light tiles (2 stages)
 //     warp 1  MMA issuer (tcgen05.mma kind::f16, A from TMEM) -- as in relight_tc.cu
 //     warp 2  TMEM allocator
-//     warps 4-7  converters: evaluate the tripling terms of their row's chunk from smem, split
-//                fp32 -> fp16 hi/lo, tcgen05.st into the A stage -- M never touches HBM
-//     warps 8-11 epilogue: drains each 16-k-block accumulation group into fp32 registers, then
-//                the per-frame scale, as in relight_tc.cu
+//     warps 4-7  converters: evaluate the tripling terms of their row's chunk from smem, scale
+//                them by 2^e (max |M| of the chunk in [2^14, 2^15)), split fp32 -> fp16 hi/lo,
+//                tcgen05.st into the A stage -- M never touches HBM
+//     warps 8-11 epilogue: drains every k block into fp32 registers with the converters'
+//                per-(row, block) power-of-two scale, then the per-frame scale, as in relight_tc.cu
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -189,12 +190,12 @@ constexpr int BM = 128, BK = 64, BN = 64;
 constexpr int DSTAGES = 3;                      // rho + V tiles
 constexpr int LSTAGES = 2;                      // light tiles
 constexpr int ASTAGES = 4;                      // TMEM A stages
-constexpr int KG = 16;                          // k-blocks per accumulation group (relight_tc.cu)
 constexpr int T_TILE = BM * BK * 4;             // 32 KB per operand tile
 constexpr int D_STAGE = 2 * T_TILE;             // rho | V
 constexpr int L_STAGE = kTcLTileBytes;          // 16 KB
 constexpr int SMEM_TILES = DSTAGES * D_STAGE + LSTAGES * L_STAGE;
-constexpr int SMEM_BYTES = SMEM_TILES + 1024 + 256;
+constexpr int EXP_OFF = SMEM_TILES + 256;       // int8 exponent ring [kExpRing][BM] after the barriers
+constexpr int SMEM_BYTES = EXP_OFF + kExpRing * BM + 1024;
 constexpr int kThreads = 384;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t ACC_COL0 = ASTAGES * 64;
@@ -217,7 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* aempty = afull + ASTAGES;                   // [ASTAGES] MMA commit -> converters
   uint64_t* tfull = aempty + ASTAGES;                   // [2] MMA -> epilogue
   uint64_t* tempty = tfull + 2;                         // [2] epilogue (128) -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* efull = tempty + 2;                         // [kExpRing] converters (128) -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(efull + kExpRing);
+  int8_t* sexp = reinterpret_cast<int8_t*>(smem + EXP_OFF);
+  static_assert((2 * DSTAGES + 2 * LSTAGES + 2 * ASTAGES + 4 + kExpRing) * 8 + 4 <= 256, "barrier block");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = K / BK;
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 128);
     }
+    for (int s = 0; s < kExpRing; ++s) mbar_init(&efull[s], 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -300,16 +305,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int lstage = 0, astage = 0;
       uint32_t lphase = 0, aphase = 0;
-      int gi = 0;   // accumulation group (KG k-blocks) counter: buffer gi & 1
+      int gi = 0;   // k-block counter: accumulator buffer gi & 1
       const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
       for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb, ++gi) {
           const int acc = gi & 1;
-          const bool first = (kb % KG) == 0;
-          if (first) {
-            mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
-            fence_after();
-          }
+          mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
           const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
           mbar_wait(&lfull[lstage], lphase);
           mbar_wait(&afull[astage], aphase);
@@ -319,11 +320,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bd = sw128_desc(lbase + kk * 32);
             const uint32_t ahi = tmem + astage * 64 + kk * 8;
-            tc_mma_ts(dhh, ahi, bd, id128, (!first || kk) ? 1u : 0u);   // [acc_hh | acc_x] += M_hi x [L_hi | L_lo]
-            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);                  // acc_x += M_lo x L_hi
+            tc_mma_ts(dhh, ahi, bd, id128, kk ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) M_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);     // acc_x += M_lo x L_hi
           }
           tc_commit(&lempty[lstage]);
           tc_commit(&aempty[astage]);
+          tc_commit(&tfull[acc]);   // block complete: the epilogue drains it into registers
           if (++lstage == LSTAGES) {
             lstage = 0;
             lphase ^= 1;
@@ -331,10 +333,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++astage == ASTAGES) {
             astage = 0;
             aphase ^= 1;
-          }
-          if ((kb % KG) == KG - 1 || kb == nkb - 1) {
-            tc_commit(&tfull[acc]);   // group complete: the epilogue drains it into registers
-            ++gi;
           }
         }
       }
@@ -347,8 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sw = row & 7;
     int stage = 0, astage = 0;
     uint32_t phase = 0, aphase = 0;
+    int gi = 0;
     for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb, ++gi) {
         mbar_wait(&dfull[stage], phase);
         mbar_wait(&aempty[astage], aphase ^ 1);
         fence_after();
@@ -359,19 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             [&](int u) { return *reinterpret_cast<const float4*>(tr + (u >> 3) * (T_TILE / 2) + (((u & 7) ^ sw) << 4)); },
             [&](int u) { return *reinterpret_cast<const float4*>(tv + (u >> 3) * (T_TILE / 2) + (((u & 7) ^ sw) << 4)); },
             w0, inv_cells, o);
+        float mx = 0.f;
+#pragma unroll
+        for (int i = 0; i < QC; ++i) mx = fmaxf(mx, fabsf(o[i]));
+        const int e = split_exponent(mx);
+        const float sc = pow2i(e);
+        const int slot = gi & (kExpRing - 1);
+        sexp[slot * BM + row] = (int8_t)e;
+        mbar_arrive(&efull[slot]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const float a = o[32 * h + 2 * c], b = o[32 * h + 2 * c + 1];
-            const __half2 hh = __floats2half2_rn(a, b);
-            const float2 hf = __half22float2(hh);
-            const float2 rr = resid2048(make_float2(a, b), hf);   // (o - hi) 2^11, exact
-            const __half2 ll = __floats2half2_rn(rr.x, rr.y);
-            hi[c] = *reinterpret_cast<const uint32_t*>(&hh);
-            lo[c] = *reinterpret_cast<const uint32_t*>(&ll);
-          }
+          for (int c = 0; c < 16; ++c) split_pair(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], sc, hi[c], lo[c]);
           tmem_st16(lane_base + astage * 64 + h * 16, hi);
           tmem_st16(lane_base + astage * 64 + 32 + h * 16, lo);
         }
@@ -401,7 +400,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-      for (int g0 = 0; g0 < nkb; g0 += KG, ++gi) {
+      for (int kb = 0; kb < nkb; ++kb, ++gi) {
+        const int slot = gi & (kExpRing - 1);
+        mbar_wait(&efull[slot], (gi / kExpRing) & 1);
+        const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row's block
         const int acc = gi & 1;
         mbar_wait(&tfull[acc], (gi >> 1) & 1);
         fence_after();
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += fmaf(xx[j], 1.f / 2048.f, hh[j]);
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] = fmaf(fmaf(xx[j], 1.f / 2048.f, hh[j]), rs, sum[c * 16 + j]);
         }
         fence_before();
         mbar_arrive(&tempty[acc]);
@@ -507,12 +509,7 @@ hs_status launch_relight_triple(const float* brdf_q, const float* vis_q, long lo
         return HS_ERR_CUDA;
       }
     }
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [] {
-      attr_err = cudaFuncSetAttribute(relight_triple_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    });
-    HS_CHECK_CUDA(attr_err, "cudaFuncSetAttribute(relight_triple_tc_kernel)");
+    HS_SMEM_ATTR(relight_triple_tc_kernel, SMEM_BYTES);
     const int ntiles = (int)((V + BM - 1) / BM);
     const long long nwork = (long long)ntiles * (batch / BN);
     const int grid = (int)(nwork < num_sms() ? nwork : num_sms());

@@ -122,6 +122,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
   float* wsf = nullptr;
   const long long wsface = (ndim == 2) ? ws_face_floats_2d(n) * 8 : 0;   // bytes per face
   if (ndim == 2) wsf = reinterpret_cast<float*>(ws);
+  if (faces < 1 || faces > kMaxFacesPerLaunch) return HS_ERR_INVALID_ARG;   // ShiftArgs holds one chunk's faces
   const long long batches = num_faces / faces;
   const long long chunk_b = std::max<long long>(1, kMaxFacesPerLaunch / faces);
   ShiftArgs a;
@@ -169,9 +170,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     } else {
       const size_t smem = (size_t)2 * (1u << n) * sizeof(double);
       if (smem > 48 * 1024) {
-        HS_CHECK_CUDA(cudaFuncSetAttribute(shift1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem),
-                      "cudaFuncSetAttribute(shift1d_kernel)");
+        HS_SMEM_ATTR(shift1d_kernel, smem);
       }
       shift1d_kernel<<<nf, k1DThreads, smem, st>>>(a);
       HS_CHECK_LAUNCH("shift1d_kernel");

@@ -736,19 +736,9 @@ __global__ void permute_kernel(const __grid_constant__ ShiftArgs args) {
 
 template <typename FT>
 hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_t st) {
-  static bool attr_done = false;  // idempotent attribute set (benign race: same value)
-  if (!attr_done) {
-    HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_tile_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_tile_smem<FT>()),
-                  "cudaFuncSetAttribute(shift2d_tile_kernel)");
-    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_fields_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kFieldsSmem),
-                  "cudaFuncSetAttribute(coarse_fields_kernel)");
-    HS_CHECK_CUDA(cudaFuncSetAttribute(coarse_finish_kernel<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kFinishSmem),
-                  "cudaFuncSetAttribute(coarse_finish_kernel)");
-    attr_done = true;
-  }
+  HS_SMEM_ATTR(shift2d_tile_kernel<FT>, max_tile_smem<FT>());
+  HS_SMEM_ATTR(coarse_fields_kernel, kFieldsSmem);
+  HS_SMEM_ATTR(coarse_finish_kernel<FT>, kFinishSmem);
   if (any_coarse) {
     coarse_fields_kernel<<<a.num_faces, kThreads, kFieldsSmem, st>>>(a);
     HS_CHECK_LAUNCH("coarse_fields_kernel");
@@ -876,12 +866,7 @@ hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_
   if (a.log2n <= kSmallMaxLog2n) {
     const size_t smem = (size_t)(1 << (2 * a.log2n)) * 4 +
                         ((size_t)3 * (1 << (2 * a.log2n)) * 2 + 3 * (1 << (2 * (a.log2n > 0 ? a.log2n - 1 : 0)))) * 8;
-    static bool attr = false;
-    if (!attr) {
-      HS_CHECK_CUDA(cudaFuncSetAttribute(shift2d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmem),
-                    "cudaFuncSetAttribute(shift2d_small_kernel)");
-      attr = true;
-    }
+    HS_SMEM_ATTR(shift2d_small_kernel, kSmallSmem);
     shift2d_small_kernel<<<a.num_faces, kThreads, smem, st>>>(a);
     HS_CHECK_LAUNCH("shift2d_small_kernel");
     return HS_OK;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
@@ -10,6 +11,7 @@
 #include <mutex>
 
 namespace hs {
+int device_sm_count();   // common.cuh: SMs of the current device, cached per device
 namespace tc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -113,16 +115,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-inline int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+inline int num_sms() { return ::hs::device_sm_count(); }
 
 // (v - h) * 2^11 for a pair, as two packed f32x2 instructions (sm_100 FADD2 / FMUL2): the same
 // roundings as the scalar form (the difference is exact, the power-of-two scale is exact)
@@ -133,6 +126,36 @@ __device__ __forceinline__ float2 resid2048(float2 v, float2 h) {
       : "=f"(r.x), "=f"(r.y)
       : "f"(v.x), "f"(v.y), "f"(h.x), "f"(h.y), "f"(2048.f));
   return r;
+}
+
+
+// ------------------------------------------------------------------------------- range handling
+// Per-(row, 64-k block) power-of-two exponents of the split-precision tensor-core relights
+// (DESIGN.md §5.3): the converter thread that owns a row scales the block's values by 2^e so that
+// their max |x| lands in [2^14, 2^15) -- the top of fp16's range -- before the hi/lo split, and
+// passes e to the epilogue through a ring of kExpRing int8 slots per row; the epilogue drains the
+// block's accumulators and multiplies them by 2^-e.  The split is then relative to the block's own
+// magnitude for every fp32 input, not just |x| in fp16's range.
+constexpr int kExpRing = 8;
+__device__ __forceinline__ int split_exponent(float mx) {
+  if (!(mx > 0.f) || !isfinite(mx)) return 0;   // zero block: any e; inf / NaN propagate unscaled
+  const int e = 14 - ilogbf(mx);
+  return e < -126 ? -126 : (e > 126 ? 126 : e);
+}
+__device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }   // e in [-126, 127]
+// fp16 hi / lo pieces of (a, b) * sc (sc a power of two: exact), lo = (x - hi) 2^11
+__device__ __forceinline__ void split_pair(float a, float b, float sc, uint32_t& hi, uint32_t& lo) {
+  float2 v;
+  asm("{\n\t.reg .b64 va, k;\n\tmov.b64 va, {%2, %3};\n\tmov.b64 k, {%4, %4};\n\t"
+      "mul.rn.f32x2 va, va, k;\n\tmov.b64 {%0, %1}, va;\n\t}"
+      : "=f"(v.x), "=f"(v.y)
+      : "f"(a), "f"(b), "f"(sc));
+  const __half2 h = __floats2half2_rn(v.x, v.y);
+  const float2 hf = __half22float2(h);
+  const float2 r = resid2048(v, hf);
+  const __half2 l = __floats2half2_rn(r.x, r.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 }  // namespace tc

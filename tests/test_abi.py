@@ -120,10 +120,10 @@ def test_widened_entries_validate_before_device(lib):
     need = lib.relight_triple_workspace_bytes(100, 6, 1024, 64)
     assert need >= 64 * 6144 * 4 and lib.relight_triple_workspace_bytes(100, 6, 16, 64) == 0   # k_face < 64
     assert t(None, FAKE, 100, 6, 1024, FAKE * 2, 1024, 64, FAKE * 4, W, need, None) == 1         # null brdf
-    assert t(FAKE, FAKE * 2, 100, 6, 16, FAKE * 3, 16, 64, FAKE * 4, W, need, None) == 1         # k_face < 64
-    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 512, 64, FAKE * 4, W, need, None) == 1      # stride < k
-    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 1024, 64, FAKE * 4, W, need - 1, None) == 1  # small ws
-    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 3, 1024, 64, FAKE * 4, W + 512, need, None) == 2  # ws align
+    assert t(FAKE, FAKE * 2, 100, 6, 16, FAKE * 8, 16, 64, FAKE * 12, W, need, None) == 1         # k_face < 64
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 8, 512, 64, FAKE * 12, W, need, None) == 1      # stride < k
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 8, 1024, 64, FAKE * 12, W, need - 1, None) == 1  # small ws
+    assert t(FAKE, FAKE * 2, 100, 6, 1024, FAKE * 8, 1024, 64, FAKE * 12, W + 512, need, None) == 2  # ws align
     pk = lib.haar_pack_qtree
     assert pk(FAKE, 4, 6, 64, 2, FAKE * 4, None) == 1                                           # log2k < 3
     assert pk(FAKE, 4, 6, 32, 3, FAKE * 4, None) == 1                                           # stride < 4^k
@@ -165,3 +165,46 @@ def test_no_device_fails_loudly(lib):
     from paper_1705_07272_b200 import _lib
     with pytest.raises(_lib.HaarShiftError):
         _lib.check("relight_vertices", st)
+
+
+def test_face_limit_and_radiance_overlap(lib):
+    """more than HS_MAX_FACES faces per batch entry is rejected (it used to overflow the
+    launch's parameter block); radiance may not overlap any input of the relight entry points."""
+    a, p = _shifts(2 * 2048)
+    W = FAKE * 64
+    big = 1 << 32
+    assert lib.haar_shift_coeffs(FAKE, big, 2, 3, 1025, 1, p, 3, W, 1 << 30, None) == 1
+    assert lib.haar_shift_coeffs(FAKE, big, 1, 3, 2048, 1, p, 3, W, 1 << 30, None) == 1
+    assert lib.haar_shift_coeffs_coarse(FAKE, big, 8, 5, 1025, 1, p, 5, W, 1 << 30, None) == 1
+    assert lib.relight_vertices_shifted(FAKE, 10, 1025, FAKE * 2, 3, FAKE * 3, FAKE * 4, W, 1 << 40, None) == 1
+    f = lib.relight_vertices
+    # radiance inside transfer / inside the light
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE + 64, None, 0, None) == 1
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 2 + 16, None, 0, None) == 1
+    g = lib.relight_vertices_shifted
+    assert g(FAKE, 10, 6, FAKE * 2, 3, FAKE * 3, FAKE + 4, W, 1 << 30, None) == 1
+    t = lib.relight_vertices_triple
+    need = lib.relight_triple_workspace_bytes(100, 6, 1024, 64)
+    assert t(FAKE, FAKE * 4, 100, 6, 1024, FAKE * 8, 1024, 64, FAKE * 4 + 256, W, need, None) == 1   # in vis_q
+    sp = lib.relight_vertices_sparse
+    assert sp(FAKE, FAKE * 2, 10, 8, FAKE * 3, 1000, 64, FAKE * 2 + 8, W, 1 << 30, None) == 1      # in values
+
+
+def test_radiance_alignment_only_where_vector_stores_run(lib):
+    """16-byte radiance alignment is required by the tensor-core epilogue only; the
+    CUDA-core paths accept any 4-byte aligned radiance (here they get past validation and fail on
+    the missing device instead of with HS_ERR_ALIGNMENT)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present: the call would run")
+    except Exception:
+        pass
+    f = lib.relight_vertices
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4 + 4, None, 0, None) in (3, 4)     # GEMV: 4-byte ok
+    assert f(FAKE, 10, 6, 16, FAKE * 2, 16, 1, FAKE * 4 + 2, None, 0, None) == 2          # not 4-byte
+    need = lib.relight_workspace_bytes(6, 1024, 64)
+    assert f(FAKE, 10, 6, 1024, FAKE * 2, 1024, 64, FAKE * 4 + 4, FAKE * 16, need, None) == 2  # tcgen05: 16
+    sp = lib.relight_vertices_sparse
+    assert sp(FAKE, FAKE * 2, 10, 8, FAKE * 3, 1000, 3, FAKE * 4 + 4, FAKE * 16, 1 << 20, None) in (3, 4)
+    assert sp(FAKE, FAKE * 2, 10, 8, FAKE * 3, 1000, 64, FAKE * 4 + 4, FAKE * 16, 1 << 20, None) == 2
