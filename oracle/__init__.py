@@ -19,15 +19,23 @@ What it computes (DESIGN.md §2 lists every reading of the pap
   product as the pixel-domain triple integral (eq:tripleSum).
 * ``rotate``: rotation of lat-long maps by the spatial ground truth: inverse,
   bilinear resampling at the rotated angles (eq:theta/eq:phi P:397-402), the azimuth shift,
-  forward; PSNR.  The GPU's chain-rule rotation approximates it (row f1): their agreement is a
-  PSNR, not a 1e-5 parity (R25).
+  forward; PSNR; and ``rotate_coeffs_chain``, the paper's own (approximate, first-order)
+  chain-rule algorithm written stage by stage.  The GPU's rotation is accurate to a PSNR against
+  the spatial truth, not to 1e-5 (R25); its 1e-5 agreement with rotate_coeffs_chain is a
+  regression check of the kernels.
 
 Everything is fp64 NumPy, written step by step with no blocking, fusion or reordering.
 Pins (tests/test_oracle_*.py, "-m 'not gpu'"): SPEC worked examples, dense
 basis-matrix brute force built from the basis definition, exact ``fractions.Fraction`` overlap
 integrals <psi_i, T_s psi_j> for 1D N=8 and 2D 4x4, closed forms (identity at 0 and N, integer
 composition, DC invariance, Parseval, linearity in the fractional part), SURVEY App. B examples.
-No function here is "parity unpinned".
+The rotation's chain-rule stages are pinned one by one (tests/test_oracle_rotate.py): the
+recursion against forward2d on exact fields, the closure (identity on exact fields, a strict
+improvement toward the analytic rotation), the DC rule's level cap by which levels can move it,
+exact cases (identity, constants, integer azimuths, the half turn) and first-order convergence to
+the analytic rotation.  Where the paper is silent (the pole rows R26, the closure and the DC rule
+R27) those pins fix the READING, not a value the paper prints: the paper gives no worked example
+of its rotation, only PSNRs of its own data (Tables 1-4).
 """
 from . import haar, shift, relight, rotate  # noqa: F401
 

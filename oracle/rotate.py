@@ -30,7 +30,8 @@ import numpy as np
 
 from . import haar, shift
 
-__all__ = ["rotated_angles", "elevate_pixels", "rotate_coeffs", "rotate_coeffs_chain", "psnr"]
+__all__ = ["rotated_angles", "elevate_pixels", "rotate_coeffs", "chain_rule_fields", "periodic_closure",
+           "fields_bottom_up", "rotated_dc", "rotate_coeffs_chain", "psnr"]
 
 
 def rotated_angles(theta, phi, alpha: float):
@@ -128,30 +129,17 @@ def _cell_means(f: np.ndarray, M: int) -> np.ndarray:
     return f.reshape(M, k, M, k).mean(axis=(1, 3))
 
 
-def rotate_coeffs_chain(c: np.ndarray, alpha: float, beta: float) -> np.ndarray:
-    """The paper's Haar-domain rotation of one N x N lat-long map (HAAR1 in, HAAR1 out), fp64:
-
-    1. the difference fields X_f, Y_f of f at the finest level with the rows across the poles (R26);
-    2. the chain rule (eq:pde1-2; Fig. 4) per output difference
-       X_g[i][j] = g(i, j) - g(i, j+1) and Y_g[i][j] = g(i, j) - g(i+1, j), g(theta, phi) =
-       f(Theta, Phi): with (Theta0, Phi0), (Theta1, Phi1) the rotated endpoints and (ThetaM, PhiM)
-       the rotated midpoint, dTheta = Theta0 - Theta1, dPhi = Phi0 - Phi1 wrapped to (-pi, pi],
-       f_Theta = -Y_f / dtheta and f_Phi = -X_f / dphi interpolated bilinearly at the midpoint
-       (X_f sits at (r, c + 1/2), Y_f at (r + 1/2, c) in pixel-centre coordinates):
-       D = f_Theta dTheta + f_Phi dPhi  (R26: increments of the two samples, not derivatives);
-    3. the periodic closure (R27): every row of X_g minus its mean; Y_g's last row = minus the sum
-       of the column's other rows;
-    4. Z_g[i][j] = X_g[i][j] - X_g[i+1][j] (R27, SPEC S:297);
-    5. the recursion h_s = [1,1], h_t = [1,2,1], decimated by 2 (eq:conv-sker P:466-478,
-       P:486-497): X_l = 1/4 (h_s along theta) (h_t along phi) X_{l+1} at even positions, Y_l the
-       transpose, Z_l = 1/4 h_t x h_t; the level-l details H = 1/4 (X[2i][2j] + X[2i+1][2j]),
-       V = 1/4 (Y[2i][2j] + Y[2i][2j+1]), D = 1/4 Z[2i][2j], times 2**-l (unit-square scale);
-    6. the scaling coefficient (R27): the mean over the N x N grid of the level-min(n, 6)
-       cell means of f sampled bilinearly at the rotated pixel centres (poles reflected);
-    7. the azimuth: the exact shift by beta N / (2 pi) columns (P:459, P:508)."""
-    f = haar.inverse2d(np.asarray(c, dtype=np.float64))
+def chain_rule_fields(f: np.ndarray, alpha: float):
+    """Step 2 of ``rotate_coeffs_chain``: the chain rule (eq:pde1-2; Fig. 4)
+    per output difference X_g[i][j] = g(i, j) - g(i, j+1) and Y_g[i][j] = g(i, j) - g(i+1, j),
+    g(theta, phi) = f(Theta, Phi), from the difference fields of the pixel map f (step 1, R26).
+    With (Theta0, Phi0), (Theta1, Phi1) the rotated endpoints and (ThetaM, PhiM) the rotated
+    midpoint, dTheta = Theta0 - Theta1, dPhi = Phi0 - Phi1 wrapped to (-pi, pi], f_Theta = -Y_f /
+    dtheta and f_Phi = -X_f / dphi interpolated bilinearly at the midpoint (X_f sits at
+    (r, c + 1/2), Y_f at (r + 1/2, c) in pixel-centre coordinates):
+    D = f_Theta dTheta + f_Phi dPhi  (R26: increments of the two samples, not derivatives).
+    Returns the raw (X_g, Y_g), N x N each."""
     N = f.shape[0]
-    n = haar.log2_exact(N)
     Xe, Ye = _fields_of_pixels(f)
     dth, dph = np.pi / N, 2.0 * np.pi / N
     I, J = np.meshgrid(np.arange(N, dtype=np.float64), np.arange(N, dtype=np.float64), indexing="ij")
@@ -168,12 +156,29 @@ def rotate_coeffs_chain(c: np.ndarray, alpha: float, beta: float) -> np.ndarray:
         dP = P0 - P1
         dP = np.where(dP > np.pi, dP - 2 * np.pi, np.where(dP < -np.pi, dP + 2 * np.pi, dP))
         out_fields.append(-yf * dT / dth - xf * dP / dph)
-    Xg, Yg = out_fields
-    Xg = Xg - Xg.mean(axis=1, keepdims=True)
-    Yg[N - 1] = -Yg[:N - 1].sum(axis=0)
-    Zg = Xg - np.roll(Xg, -1, axis=0)
+    return out_fields[0], out_fields[1]
+
+
+def periodic_closure(Xg: np.ndarray) -> np.ndarray:
+    """Step 3 (R27): the exact X field of any periodic N x N map sums to 0 along every row
+    (a telescoping sum of periodic differences); the chain rule's does not, so each row of X_g
+    loses its mean -- the orthogonal projection onto the fields that can be differences of a map.
+    (Y_g needs no closure: its last row feeds only the level-0 residual of the recursion, never
+    an output coefficient -- pinned in tests/test_oracle_rotate.py.)"""
+    return Xg - Xg.mean(axis=1, keepdims=True)
+
+
+def fields_bottom_up(Xg: np.ndarray, Yg: np.ndarray):
+    """Steps 4-5: Z_g[i][j] = X_g[i][j] - X_g[i+1][j] (R27) and the recursion
+    h_s = [1,1], h_t = [1,2,1], decimated by 2 (eq:conv-sker P:466-478):
+    X_l = 1/4 (h_s along theta) (h_t along phi) X_{l+1} at even positions, Y_l the transpose,
+    Z_l = 1/4 h_t x h_t; the level-l details H = 1/4 (X[2i][2j] + X[2i+1][2j]),
+    V = 1/4 (Y[2i][2j] + Y[2i][2j+1]), D = 1/4 Z[2i][2j], times 2**-l (unit-square scale).
+    Returns (details[0..n-1] as (H, V, D), the level-0 residuals (X_0, Y_0, Z_0))."""
+    N = Xg.shape[0]
+    n = haar.log2_exact(N)
     details = [None] * n
-    X, Y, Z = Xg, Yg, Zg
+    X, Y, Z = Xg, Yg, Xg - np.roll(Xg, -1, axis=0)
     for l in range(n - 1, -1, -1):
         s = 2.0 ** (-l)
         H = 0.25 * (X[0::2, 0::2] + X[1::2, 0::2]) * s
@@ -189,9 +194,22 @@ def rotate_coeffs_chain(c: np.ndarray, alpha: float, beta: float) -> np.ndarray:
         X = 0.25 * ht(hs(X, 0), 1)[0::2, 0::2]
         Y = 0.25 * hs(ht(Y, 0), 1)[0::2, 0::2]
         Z = 0.25 * ht(ht(Z, 0), 1)[0::2, 0::2]
-    L = min(n, 6)
-    M = 1 << L
+    return details, (float(X[0, 0]), float(Y[0, 0]), float(Z[0, 0]))
+
+
+DC_LEVEL = 6   # R27: the scaling coefficient comes from the level-min(n, 6) approximation
+
+
+def rotated_dc(f: np.ndarray, alpha: float) -> float:
+    """Step 6 (R27): the mean over the N x N grid of the level-min(n, DC_LEVEL) cell means
+    of f sampled bilinearly at the rotated pixel centres (poles reflected, phi periodic)."""
+    N = f.shape[0]
+    n = haar.log2_exact(N)
+    M = 1 << min(n, DC_LEVEL)
     A = _cell_means(f, M)
+    dth, dph = np.pi / N, 2.0 * np.pi / N
+    I, J = np.meshgrid(np.arange(N, dtype=np.float64), np.arange(N, dtype=np.float64), indexing="ij")
+    T0, P0 = rotated_angles((I + 0.5) * dth, (J + 0.5) * dph, alpha)
     y = T0 * M / np.pi - 0.5
     x = P0 * M / (2.0 * np.pi) - 0.5
     y0 = np.floor(y).astype(np.int64)
@@ -206,7 +224,24 @@ def rotate_coeffs_chain(c: np.ndarray, alpha: float, beta: float) -> np.ndarray:
             r = np.where(top, -1 - r, np.where(bot, 2 * M - 1 - r, r))
             cc = np.where(top | bot, cc + M // 2, cc)
             dc += wyv * wxv * A[r, np.mod(cc, M)]
-    coeffs = haar.pack2d(float(dc.mean()), details)
+    return float(dc.mean())
+
+
+def rotate_coeffs_chain(c: np.ndarray, alpha: float, beta: float) -> np.ndarray:
+    """The paper's Haar-domain rotation of one N x N lat-long map (HAAR1 in, HAAR1 out), fp64:
+
+    1. the difference fields X_f, Y_f of f at the finest level with the rows across the poles (R26);
+    2. the chain rule per output difference (``chain_rule_fields``);
+    3. the periodic closure of X_g (``periodic_closure``, R27);
+    4-5. Z_g and the [1,1] x [1,2,1] recursion to every detail level (``fields_bottom_up``);
+    6. the scaling coefficient (``rotated_dc``, R27);
+    7. the azimuth: the exact shift by beta N / (2 pi) columns (P:459, P:508)."""
+    f = haar.inverse2d(np.asarray(c, dtype=np.float64))
+    N = f.shape[0]
+    Xg, Yg = chain_rule_fields(f, alpha)
+    Xg = periodic_closure(Xg)
+    details, _ = fields_bottom_up(Xg, Yg)
+    coeffs = haar.pack2d(rotated_dc(f, alpha), details)
     return shift.shift_coeffs2d(coeffs, 0.0, beta * N / (2.0 * np.pi))
 
 

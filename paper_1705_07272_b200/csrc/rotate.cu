@@ -19,8 +19,9 @@
 //                        f_Phi = -X_f / dphi interpolated bilinearly at the rotated midpoint
 //                        (Fig. 4; R26 -- increments instead of derivatives
 //                        keep the poles of the source finite);
-//   rot_closure_kernel   the periodic closure the Haar fields satisfy (rows of X and columns of Y
-//                        sum to zero; the Y row across the pole wrap is the negative column sum);
+//   rot_closure_kernel   the periodic closure the Haar fields satisfy: every row of X sums to zero
+//                        (Y needs none -- its last row reaches no output coefficient, only the
+//                        recursion's level-0 residual; tests/test_oracle_rotate.py);
 //   rot_bottomup_kernel  (3) the paper's recursion h_s = [1,1], h_t = [1,2,1], decimated by 2
 //                        (eq:conv-sker P:466-478) from (X_g, Y_g, Z_g = X_g[i] - X_g[i+1])
 //                        at the finest level down to level 0: every detail coefficient of g;
@@ -234,13 +235,11 @@ __global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const double* 
   }
 }
 
-// closure: rows of X_g sum to 0 (subtract the row mean); column j of Y_g: last row = -sum of the
-// others.  One CTA per map; a warp per row (coalesced), a thread per column (coalesced).
+// closure: rows of X_g sum to 0 (subtract the row mean).  One CTA per map, a warp per row.
 __global__ void rot_closure_kernel(double* __restrict__ Gf, int n) {
   const int N = 1 << n;
   const long long NN = 1ll << (2 * n);
   double* X = Gf + (long long)blockIdx.x * 2 * NN;
-  double* Y = X + NN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = warp; r < N; r += nw) {
     double sx = 0.0;
@@ -249,11 +248,6 @@ __global__ void rot_closure_kernel(double* __restrict__ Gf, int n) {
     for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
     const double mx = sx / (double)N;
     for (int t = lane; t < N; t += 32) X[r * N + t] -= mx;
-  }
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    double sy = 0.0;
-    for (int t = 0; t < N - 1; ++t) sy += Y[t * N + k];
-    Y[(N - 1) * N + k] = -sy;
   }
 }
 

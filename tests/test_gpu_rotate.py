@@ -1,16 +1,19 @@
 """Rotation of lat-long maps in the Haar domain on the GPU (-m gpu).
 
-Parity: the GPU equals oracle.rotate.rotate_coeffs_chain (the paper's algorithm step by step in
-fp64, pinned in tests/test_oracle_rotate.py) within rel-L2 1e-5, for smooth and white-noise maps,
-random elevations (poles crossed) and azimuths, N = 8 .. 128.
-
-Accuracy of the method (the chain rule is first order, R25):
+Accuracy of the method -- the headline for f1, as the paper reports it (PSNR against rotating in
+the spatial domain):
 * alpha = 0 reproduces the input (rel-L2 <= 1e-5) and an integer azimuth is the exact column
-  permutation of the oracle (rel-L2 <= 1e-5) -- the exact parts;
-* for alpha != 0 the result is compared with the spatial ground truth (oracle.rotate: bilinear
-  resampling at the rotated angles) and with the analytic rotation of the smooth maps, as
-  PSNR, with floors set from the measured values; the PSNR must rise with the
-  resolution (the chain rule is first order in the pixel size).
+  permutation of the spatial oracle (rel-L2 <= 1e-5) -- the exact parts;
+* for alpha != 0 the GPU result is compared, as PSNR, with the spatial ground truth (oracle.rotate:
+  bilinear resampling at the rotated angles) and with the analytic rotation of the smooth maps.
+  The floors are not measured values: the GPU must be as accurate as the paper's algorithm itself
+  (oracle.rotate.rotate_coeffs_chain, fp64) to within 0.1 dB, and its PSNR against the analytic
+  rotation must rise with the resolution (the chain rule is first order in the pixel size).
+
+Regression check: the GPU equals rotate_coeffs_chain (the paper's algorithm step by step in fp64,
+each stage pinned in tests/test_oracle_rotate.py) within rel-L2 1e-5, for smooth and white-noise
+maps, random elevations (poles crossed) and azimuths, N = 2 .. 2048 (the DC's level cap binds at
+N >= 128).  That agreement shows the kernels implement the algorithm; it is not an accuracy claim.
 """
 import math
 
@@ -70,27 +73,31 @@ def _psnr_pix(a, ref):
 
 
 def test_psnr_against_spatial_and_analytic_ground_truth():
-    """GPU chain-rule rotation vs the spatial oracle (the paper's ground truth) and both
-    vs the analytic rotation of the smooth maps; floors set from the measured values."""
+    """GPU chain-rule rotation vs the spatial oracle (the paper's ground truth) and vs the
+    analytic rotation of the smooth maps.  Floors from principle, not from measurements: within
+    0.1 dB of the fp64 algorithm (rotate_coeffs_chain) against the same truths, and rising with N"""
     from oracle import haar
-    res = {}
-    for n in (5, 6, 7):
+    med_gt = {}
+    for n in (5, 6, 7, 8):
         c = synth.smooth_sphere_maps(13, 6, n)
         ang = synth.rotation_angles(14, 6)
         got = _rot(c, ang)
-        p_or, p_gt, p_ot = [], [], []
+        p_or, p_gt, q_or, q_gt = [], [], [], []
         for b in range(6):
             ref = orot.rotate_coeffs(c[b], *ang[b])
+            chain = orot.rotate_coeffs_chain(c[b], *ang[b])
             truth = _truth(13, b, n, *ang[b])
             p_or.append(orot.psnr(got[b], ref))
+            q_or.append(orot.psnr(chain, ref))
             p_gt.append(_psnr_pix(haar.inverse2d(got[b]), truth))
-            p_ot.append(_psnr_pix(haar.inverse2d(ref), truth))
-        res[n] = (min(p_or), min(p_gt), float(np.median(p_gt)), float(np.median(p_ot)))
-        print(f"n={n}: vs oracle min {min(p_or):.1f} median {np.median(p_or):.1f} dB | vs analytic: GPU min "
-              f"{min(p_gt):.1f} median {np.median(p_gt):.1f} dB, oracle median {np.median(p_ot):.1f} dB")
-    # measured (one B200): vs oracle min 33.3 / 35.6 / 38.4 dB, vs analytic median 35.9 / 41.9 / 46.0 dB
-    assert res[5][0] >= 30.0 and res[6][0] >= 32.0 and res[7][0] >= 35.0
-    assert res[5][2] < res[6][2] < res[7][2]
+            q_gt.append(_psnr_pix(haar.inverse2d(chain), truth))
+        med_gt[n] = float(np.median(p_gt))
+        print(f"n={n}: vs spatial oracle GPU min {min(p_or):.1f} median {np.median(p_or):.1f} dB "
+              f"(fp64 algorithm min {min(q_or):.1f}) | vs analytic GPU min {min(p_gt):.1f} median "
+              f"{np.median(p_gt):.1f} dB (fp64 algorithm median {np.median(q_gt):.1f})")
+        for b in range(6):
+            assert p_or[b] >= q_or[b] - 0.1 and p_gt[b] >= q_gt[b] - 0.1, (n, b)
+    assert med_gt[5] < med_gt[6] < med_gt[7] < med_gt[8]
 
 
 @pytest.mark.parametrize("n,kind", [(1, "noise"), (2, "noise"), (3, "smooth"), (4, "noise"), (5, "smooth"),

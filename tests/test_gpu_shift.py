@@ -62,8 +62,9 @@ def test_c1_2d_all_shifts_4x4():
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_2d_every_size_mixed_shifts(n):
-    """White-noise pyramids up to N = 256; N = 512 uses HDR-shaped light (DESIGN.md §4.1 error
-    model: on white-noise pyramids the fp32 difference domain exceeds 1e-5 beyond N = 256)."""
+    """White-noise pyramids at every size N = 2 .. 512 (the fields are fp64 at every size, so the
+    N = 512 case no longer needs the HDR-shaped light a round-1 fp32 build fell back to); HDR-
+    shaped light at N = 512 as well."""
     N = 1 << n
     rng = np.random.default_rng(100 + n)
     shifts = [(0, 0), (N, -N), (1, 0), (0, 1), (N // 2, 0), (0, N // 4 if N >= 4 else 1), (3.3, -1.6),
@@ -71,10 +72,10 @@ def test_2d_every_size_mixed_shifts(n):
     shifts += [tuple(x) for x in rng.uniform(-2 * N, 2 * N, size=(6, 2))]
     shifts += [tuple(x) for x in rng.integers(-N, 2 * N, size=(4, 2)).astype(float)]
     B, F = len(shifts), 2
-    if n <= 8:
-        coeffs = synth.random_signals(200 + n, B * F, N * N).reshape(B, F, N * N)
-    else:
-        coeffs = synth.light_pyramids(200 + n, B, F, n)
+    coeffs = synth.random_signals(200 + n, B * F, N * N).reshape(B, F, N * N)
+    if n >= 9:   # both kinds at the largest size of this sweep
+        coeffs = np.concatenate([coeffs, synth.light_pyramids(200 + n, B, F, n)], axis=1)
+        F = 2 * F
     sh = np.broadcast_to(np.array(shifts, dtype=np.float64)[:, None, :], (B, F, 2)).copy()
     got = _run(coeffs, sh, 2)
     ref = oshift.shift_coeffs(coeffs, sh, 2)

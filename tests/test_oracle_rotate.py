@@ -6,7 +6,12 @@
   itself upside down with phi mirrored through pi (closed form);
 * rotate_coeffs: alpha = 0 with an integer azimuth shift is the exact circular column shift of the
   pixel map (S:199), and alpha = 0, beta = 0 is the identity on coefficients;
-* synth.smooth_sphere_maps equals the forward transform of its closed-form cell means.
+* synth.smooth_sphere_maps equals the forward transform of its closed-form cell means;
+* the chain-rule algorithm (rotate_coeffs_chain): exact cases (identity, constants, integer
+  azimuths, the half turn), convergence to the analytic rotation, and each stage on its own --
+  the recursion against forward2d on exact fields, the periodic closure (identity on exact fields,
+  a strict improvement toward the analytic rotation, applied inside the chain), the dead last
+  row of Y, and the DC rule's level cap (reads exactly the levels below min(n, 6)).
 """
 import math
 
@@ -148,3 +153,157 @@ def test_chain_converges_to_the_analytic_rotation():
     print(med)
     assert med[0] < med[1] < med[2]
     assert med[0] >= 28.0 and med[1] >= 34.0 and med[2] >= 40.0
+
+
+# ------------------------------------------- the chain-rule stages pinned one by one
+
+def _exact_fields(g):
+    """periodic difference fields of a pixel map: X = g - g(c+1), Y = g - g(r+1)"""
+    return g - np.roll(g, -1, axis=1), g - np.roll(g, -1, axis=0)
+
+
+def test_bottom_up_of_exact_fields_is_the_forward_transform():
+    """step 5 alone: on the exact periodic fields of any map the [1,1] x [1,2,1] recursion returns
+    that map's Haar details -- pinned against forward2d (itself pinned by the basis brute force) --
+    and the level-0 residuals vanish"""
+    rng = np.random.default_rng(31)
+    for n in (1, 2, 3, 5, 7):
+        g = rng.normal(size=(1 << n, 1 << n))
+        details, res = rotate.fields_bottom_up(*_exact_fields(g))
+        got = haar.pack2d(float(g.mean()), details)
+        np.testing.assert_allclose(got, haar.forward2d(g), atol=1e-12)
+        np.testing.assert_allclose(res, 0.0, atol=1e-9)
+
+
+def test_last_row_of_y_never_reaches_an_output():
+    """why Y_g needs no closure (R27): its last row enters only the odd rows of every
+    coarser Y, which no V detail reads -- any value there changes the level-0 residual alone"""
+    rng = np.random.default_rng(32)
+    for n in (3, 6):
+        X, Y = _exact_fields(rng.normal(size=(1 << n, 1 << n)))
+        d0, r0 = rotate.fields_bottom_up(X, Y)
+        Y2 = Y.copy()
+        Y2[-1] = rng.normal(size=1 << n) * 100.0
+        d1, r1 = rotate.fields_bottom_up(X, Y2)
+        for a, b in zip(d0, d1):
+            for u, v in zip(a, b):
+                np.testing.assert_array_equal(u, v)
+        assert abs(r1[1] - r0[1]) > 1.0
+
+
+def test_closure_is_the_identity_on_exact_fields_and_zeroes_row_sums():
+    """step 3: the exact X field of a periodic map already sums to 0 along each row (a telescoping
+    sum), so the closure leaves it unchanged (a closure on the wrong axis, a wrong sign or scale
+    would not); on the chain rule's raw field it removes nonzero row sums"""
+    rng = np.random.default_rng(33)
+    g = rng.normal(size=(32, 32))
+    X, _ = _exact_fields(g)
+    np.testing.assert_allclose(rotate.periodic_closure(X), X, atol=1e-13)
+    f = haar.inverse2d(synth.smooth_sphere_maps(34, 1, 5)[0].astype(np.float64))
+    Xr, _ = rotate.chain_rule_fields(f, 0.9)
+    assert np.abs(Xr.sum(axis=1)).max() > 1e-4
+    np.testing.assert_allclose(rotate.periodic_closure(Xr).sum(axis=1), 0.0, atol=1e-12)
+
+
+def _analytic_point_fields(seed, k, n, alpha):
+    """exact X field of the rotated analytic map sampled at pixel centres"""
+    N = 1 << n
+    th = (np.arange(N) + 0.5) * np.pi / N
+    ph = (np.arange(N) + 0.5) * 2 * np.pi / N
+    T, P = np.meshgrid(th, ph, indexing="ij")
+    Th, Ph = rotate.rotated_angles(T, P, alpha)
+    g = synth.smooth_sphere_eval(seed, k, Th, Ph)
+    return g - np.roll(g, -1, axis=1)
+
+
+def test_closure_moves_chain_fields_toward_the_exact_rotation():
+    """the reason for R27: the exact rotated field has zero row sums, so projecting the chain
+    rule's raw field onto zero-row-sum fields strictly reduces its distance to the truth (the
+    analytic map rotated exactly, sampled at the pixel centres) -- the raw row sums are pure error"""
+    for n in (5, 6):
+        c = synth.smooth_sphere_maps(35, 3, n)
+        ang = synth.rotation_angles(36, 3)
+        for b in range(3):
+            f = haar.inverse2d(c[b].astype(np.float64))
+            Xr, _ = rotate.chain_rule_fields(f, ang[b][0])
+            Xt = _analytic_point_fields(35, b, n, ang[b][0])
+            e_raw = np.linalg.norm(Xr - Xt)
+            e_closed = np.linalg.norm(rotate.periodic_closure(Xr) - Xt)
+            assert e_closed < e_raw * (1 - 1e-6), (n, b, e_raw, e_closed)
+
+
+def test_chain_is_the_composition_of_its_stages():
+    """rotate_coeffs_chain applies every stage (a dropped closure or a different DC rule fails
+    here): the composition written out from the pinned stages, and the same without the closure
+    differs"""
+    c = synth.smooth_sphere_maps(37, 2, 5)
+    ang = synth.rotation_angles(38, 2)
+    for b in range(2):
+        f = haar.inverse2d(c[b].astype(np.float64))
+        Xr, Yr = rotate.chain_rule_fields(f, ang[b][0])
+        N = f.shape[0]
+        sh = ang[b][1] * N / (2 * np.pi)
+        d, _ = rotate.fields_bottom_up(rotate.periodic_closure(Xr), Yr)
+        want = shift_coeffs2d(haar.pack2d(rotate.rotated_dc(f, ang[b][0]), d), 0.0, sh)
+        got = rotate.rotate_coeffs_chain(c[b], *ang[b])
+        np.testing.assert_allclose(got, want, atol=1e-12)
+        d_open, _ = rotate.fields_bottom_up(Xr, Yr)
+        unclosed = shift_coeffs2d(haar.pack2d(rotate.rotated_dc(f, ang[b][0]), d_open), 0.0, sh)
+        assert np.abs(unclosed - got).max() > 1e-6
+
+
+def shift_coeffs2d(c, sy, sx):
+    from oracle import shift
+    return shift.shift_coeffs2d(c, sy, sx)
+
+
+def _perturbed_dc(c, level, alpha, rng):
+    """rotated_dc of the map before and after a random change of one detail coefficient at `level`"""
+    n = haar.log2_exact(int(round(np.sqrt(c.size))))
+    idx = 4 ** level * (1 + rng.integers(0, 3)) + rng.integers(0, 4 ** level)
+    d = c.astype(np.float64).copy()
+    d[idx] += 0.5
+    return (rotate.rotated_dc(haar.inverse2d(c.astype(np.float64)), alpha),
+            rotate.rotated_dc(haar.inverse2d(d), alpha))
+
+
+def test_dc_reads_exactly_the_levels_below_six():
+    """R27 / S:301: the scaling coefficient is the mean of the level-min(n, 6) approximation
+    resampled at the rotated pixel centres.  So at n = 7 and 8 (where the cap binds) no detail at
+    level >= 6 can move it, while every coarser level does (a rule reading level 5 or level n
+    fails one of the two); at n = 5 every level moves it"""
+    rng = np.random.default_rng(39)
+    for n in (7, 8):
+        c = synth.smooth_sphere_maps(40, 1, n)[0]
+        for level in (6, n - 1):
+            a, b = _perturbed_dc(c, level, 0.7, rng)
+            assert abs(a - b) <= 1e-13 * abs(a), (n, level)
+        for level in (5, 3):
+            a, b = _perturbed_dc(c, level, 0.7, rng)
+            assert abs(a - b) > 1e-7, (n, level, a, b)
+    c = synth.smooth_sphere_maps(41, 1, 5)[0]
+    for level in (4, 2):
+        a, b = _perturbed_dc(c, level, 0.7, rng)
+        assert abs(a - b) > 1e-7
+
+
+def test_dc_exact_cases():
+    """alpha = 0 samples every cell at its centre: the DC is the map's mean exactly, at every n
+    (including n > 6, where the level-6 cell means average to the same mean); a constant stays"""
+    for n in (3, 6, 8):
+        c = synth.smooth_sphere_maps(42, 1, n)[0].astype(np.float64)
+        f = haar.inverse2d(c)
+        assert abs(rotate.rotated_dc(f, 0.0) - c[0]) < 1e-12
+        assert abs(rotate.rotated_dc(np.full_like(f, 3.25), 1.234) - 3.25) < 1e-12
+
+
+def test_chain_output_dc_ignores_fine_levels():
+    """end to end at n = 8: changing level-6 and level-7 details of the input leaves the output's
+    scaling coefficient unchanged"""
+    rng = np.random.default_rng(43)
+    c = synth.smooth_sphere_maps(44, 1, 8)[0].astype(np.float64)
+    d = c.copy()
+    d[4 ** 6:] += rng.normal(size=c.size - 4 ** 6) * 0.01
+    a = rotate.rotate_coeffs_chain(c, 0.6, 1.0)[0]
+    b = rotate.rotate_coeffs_chain(d, 0.6, 1.0)[0]
+    assert abs(a - b) <= 1e-13 * abs(a)          # fp64 rounding of the cell means only
