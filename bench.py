@@ -134,28 +134,40 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------ oracle arm
 
-def oracle_sample(cfg, frames_sample=1, rows_sample=4000, seed_off=0):
-    """Time the fp64 oracle on a bounded sample of the step; returns (seconds for the FULL step,
-    extrapolated linearly from the sample, sample description, threads)."""
+def oracle_sample(cfg, den=16, seed_off=0):
+    """Time the fp64 oracle on 1/den of the step's workload: the shift of frames/den frames (at
+    least one) and the relight of vertices/den vertex rows x all frames.  Returns (measured
+    seconds, vertices in the sample, description).  The sample rate (sample vertices / measured
+    time) equals the full step's rate when the oracle scales linearly in frames and rows; nothing
+    is extrapolated into the reported step time."""
     from oracle import relight as orelight
     from oracle import shift as oshift
-    N = 1 << cfg.log2n
-    light = synth.light_pyramids(cfg.seed, frames_sample, cfg.faces, cfg.log2n)
-    s = synth.c5_shifts(cfg.seed, cfg.frames, cfg.log2n)[:frames_sample]
-    sh = np.broadcast_to(s[:, None, :], (frames_sample, cfg.faces, 2))
+    N, F, kf = 1 << cfg.log2n, cfg.faces, cfg.k_face
+    frames_s = max(1, cfg.frames // den)
+    rows_s = max(1, cfg.vertices // den)
+    light = synth.light_pyramids(cfg.seed, frames_s, F, cfg.log2n)
+    s = synth.c5_shifts(cfg.seed, cfg.frames, cfg.log2n)[:frames_s]
+    sh = np.broadcast_to(s[:, None, :], (frames_s, F, 2))
+    if cfg.name == "c5t":
+        rows = (synth.shading_rows(cfg.seed, seed_off, rows_s, F, kf, synth.STREAM_BRDF),
+                synth.shading_rows(cfg.seed, seed_off, rows_s, F, kf, synth.STREAM_VIS))
+    else:
+        rows = (synth.transfer_rows(cfg.seed, seed_off, rows_s, F, kf),)
     t0 = time.perf_counter()
     shifted = oshift.shift_coeffs(light, sh, 2)
     t_shift = time.perf_counter() - t0
-    T = synth.transfer_rows(cfg.seed, seed_off, rows_sample, cfg.faces, cfg.k_face)
-    Lb = np.concatenate([shifted] * (cfg.frames // frames_sample + 1))[: cfg.frames]
+    Lb = np.concatenate([shifted] * (cfg.frames // frames_s + 1))[: cfg.frames]
     t0 = time.perf_counter()
-    orelight.relight(T, Lb, cfg.faces, cfg.k_face)
+    if cfg.name == "c5t":
+        orelight.relight_triple(rows[0], rows[1], Lb, F, kf)
+    else:
+        orelight.relight(rows[0], Lb, F, kf)
     t_rel = time.perf_counter() - t0
-    full = t_shift * (cfg.frames / frames_sample) + t_rel * (cfg.vertices / rows_sample)
-    desc = (f"oracle fp64: shift of {frames_sample}/{cfg.frames} frames x {cfg.faces} faces of {N}x{N} "
-            f"({t_shift:.3f}s) + relight of {rows_sample}/{cfg.vertices} vertex rows x {cfg.frames} frames "
-            f"({t_rel:.3f}s); step time extrapolated linearly to the full workload")
-    return full, desc
+    what = "triple product" if cfg.name == "c5t" else "relight"
+    desc = (f"oracle fp64 on 1/{den} of the step, measured (not extrapolated): shift of {frames_s}/{cfg.frames} "
+            f"frames x {F} faces of {N}x{N} ({t_shift:.3f}s) + {what} of {rows_s}/{cfg.vertices} vertex rows x "
+            f"{cfg.frames} frames ({t_rel:.3f}s); value = sample vertices / measured time")
+    return t_shift + t_rel, rows_s, desc
 
 
 def cpu_threads():
@@ -174,20 +186,20 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    V = cfg.vertices
     warm, steps = max(args.warmup, 0), max(args.steps, 1)
+    ref_den = 256 if cfg.name == "c5t" else 16     # the triple-product oracle is ~60x slower per vertex
     times = []
-    sampler = oracle_sample_triple if cfg.name == "c5t" else oracle_sample
     for i in range(warm + steps):
-        full, desc = sampler(cfg, 1, 20000, seed_off=i * 20000)
+        t, rows_s, desc = oracle_sample(cfg, ref_den, seed_off=(i * 997) % max(1, cfg.vertices))
         if i >= warm:
-            times.append(full)
+            times.append(t)
     t = statistics.median(times)
-    value = V / t
+    value = rows_s / t
     cores = cpu_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "step": f"1/{ref_den} of the workload per step ({rows_s} vertices); ms_per_step is that measured sample step",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -247,6 +259,7 @@ def run_ours(args, cfg):
         ws = torch.empty(max(1, hs.haar_shift_workspace_bytes(2, n, F, max(fsn, 1))), dtype=torch.uint8, device=dev)
     gather_mode = args.gather if world > 1 else "none"
     R_view = None
+    fence_flag = torch.zeros(1, dtype=torch.int32, device=dev)
     if gather_mode == "p2p":
         # fused relight + gather: every rank's relight epilogue stores straight into rank 0's buffer
         try:
@@ -292,8 +305,7 @@ def run_ours(args, cfg):
             hsdist.allgather_band(band_local, shifted)
             if gather_mode == "p2p":
                 hsdist.relight_into_peer(T, shifted, V, relight_fn, R_view)
-                stream.synchronize()
-                dist.barrier()              # every rank's rows are in rank 0's buffer
+                hsdist.rows_landed_fence(fence_flag)   # stream-ordered: rank 0's later work sees every row
                 return R_full
             _, full = hsdist.relight_and_gather(T, shifted, V, relight_fn, R_full, chunks=args.chunks)
             return full
@@ -383,37 +395,42 @@ def run_ours(args, cfg):
                        f"relight ({args.e2e_chunks} chunks) with each chunk's radiance D2H overlapped; T is scene "
                        "data resident in HBM"}
     elif not args.no_e2e:
+        # N > 1 host buffers: each rank H2Ds its own frames, shifts them, the band is all-gathered,
+        # and each rank D2Hs its own radiance rows, chunked under its relight, into ONE shared
+        # page-locked host array (all N PCIe links carry the gather)
+        from paper_1705_07272_b200.pipeline import ShardedShiftRelightPipeline
         light_h = torch.from_numpy(light_np).pin_memory()
-        out_rows = V if rank == 0 else 0
-        Rh = torch.empty((out_rows, B), dtype=torch.float32).pin_memory()
-
-        def e2e_step():
-            light[fs0:fs0 + fsn].copy_(light_h[fs0:fs0 + fsn], non_blocking=True)   # this rank's frames
-            res = step()
-            if res is not None and rank == 0:
-                Rh.copy_(res, non_blocking=True)
-
+        shared = hsdist.SharedHostBuffer((V, B))
+        pipe = ShardedShiftRelightPipeline(T, F, n, B, cfg.band_levels, V, chunks=args.e2e_chunks)
         for _ in range(max(1, args.warmup)):
-            e2e_step()
+            pipe.step(light_h, shifts, shared.tensor)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            e2e_step()
+            ev = pipe.step(light_h, shifts, shared.tensor)
+        stream.wait_event(ev)
         b.record(stream)
         torch.cuda.synchronize()
         e_ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        if rank == 0:   # the shared host array holds every rank's rows: spot-check against one rank's device rows
+            ok = bool(torch.equal(shared.tensor[: pipe.R.shape[0]], pipe.R.cpu()))
+        shared.close()
+        bytes_io = torch.tensor([pipe.h2d_bytes(), pipe.d2h_bytes()], dtype=torch.float64, device=dev)
+        dist.all_reduce(bytes_io)
         e2e = {"value": V / (float(e_ms.item()) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(light_np[fs0:fs0 + fsn].nbytes),
-               "d2h_bytes_per_step": int(out_rows * B * 4),
-               "note": "per step: pinned H2D of each rank's own light frames (rank 0's bytes shown) + sharded "
-                       "shift + band all-gather + relight + gather + D2H of the full radiance on rank 0; T is "
-                       "scene data resident in HBM"}
+               "h2d_bytes_per_step": int(bytes_io[0].item()), "d2h_bytes_per_step": int(bytes_io[1].item()),
+               "ms_per_step": float(e_ms.item()),
+               "note": "ShardedShiftRelightPipeline.step per step on every rank: pinned H2D of the rank's own "
+                       "light frames, sharded shift, band all-gather (NCCL), chunked relight of the rank's rows "
+                       "with each chunk's D2H into one shared page-locked host array (bytes summed over ranks); "
+                       "T is scene data resident in HBM"}
+        if rank == 0:
+            e2e["rank0_rows_match_device"] = ok
 
     if rank == 0:
         line = {
@@ -422,9 +439,11 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "arithmetic": "fp32 in / out; shift fields fp64; relight: fp32 GEMV (B <= 8) or tcgen05 products of "
                           "fp16 hi/lo splits accumulated in fp32 (B % 64 == 0), within 1e-5 of the fp64 oracle",
-            "config": {**workload_config(cfg, world), "gather": gather_mode},
+            "config": workload_config(cfg, world),
+            "gather": gather_mode,
             "vertex_frames_per_sec": V * B / (ms_max * 1e-3),
-            "shift_coeffs_per_sec": B * F * N * N / (ms_max * 1e-3),
+            "shift_coeffs_per_sec": (B * F * N * N / (statistics.median([a.elapsed_time(b) for a, b in shift_events])
+                                                       * 1e-3)) if shift_events else None,
             "roofline": {"bound": "hbm", "kernel": "relight_vertices", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes),
@@ -439,9 +458,10 @@ def run_ours(args, cfg):
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:
-            # ~4 s of fp64 BLAS at K = 6144; fewer rows for longer transfer rows (host memory)
-            full, desc = oracle_sample(cfg, 16, max(2000, 400000 * 6144 // (cfg.faces * cfg.k_face)))
-            line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+            # a few seconds of fp64 work: 1/4 of the step at K = 6144, less for longer transfer rows
+            den = 4 * max(1, (cfg.faces * cfg.k_face) // 6144)
+            t_s, rows_s, desc = oracle_sample(cfg, den)
+            line["cpu_baseline"] = {"value": rows_s / t_s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                                     "sample": desc}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -854,31 +874,6 @@ def fill_shading(hs, out, r0, faces, kf, seed, stream):
     out[:, ::kf] = sc
 
 
-def oracle_sample_triple(cfg, frames_sample=1, rows_sample=4000, seed_off=0):
-    """The oracle on a bounded sample of the c5t step (shift of frames_sample frames, triple
-    product of rows_sample vertices x all frames), extrapolated linearly to the full step."""
-    from oracle import relight as orelight
-    from oracle import shift as oshift
-    N, F, kf = 1 << cfg.log2n, cfg.faces, cfg.k_face
-    light = synth.light_pyramids(cfg.seed, frames_sample, F, cfg.log2n)
-    s = synth.c5_shifts(cfg.seed, cfg.frames, cfg.log2n)[:frames_sample]
-    sh = np.broadcast_to(s[:, None, :], (frames_sample, F, 2))
-    t0 = time.perf_counter()
-    shifted = oshift.shift_coeffs(light, sh, 2)
-    t_shift = time.perf_counter() - t0
-    rho = synth.shading_rows(cfg.seed, seed_off, rows_sample, F, kf, synth.STREAM_BRDF)
-    vis = synth.shading_rows(cfg.seed, seed_off, rows_sample, F, kf, synth.STREAM_VIS)
-    Lb = np.concatenate([shifted] * (cfg.frames // frames_sample + 1))[: cfg.frames]
-    t0 = time.perf_counter()
-    orelight.relight_triple(rho, vis, Lb, F, kf)
-    t_rel = time.perf_counter() - t0
-    full = t_shift * (cfg.frames / frames_sample) + t_rel * (cfg.vertices / rows_sample)
-    desc = (f"oracle fp64: shift of {frames_sample}/{cfg.frames} frames x {F} faces of {N}x{N} ({t_shift:.3f}s) + "
-            f"triple product of {rows_sample}/{cfg.vertices} vertices x {cfg.frames} frames ({t_rel:.3f}s); "
-            "step time extrapolated linearly to the full workload")
-    return full, desc
-
-
 def run_triple(args, cfg):
     """c5t (row f3): shift 64 frames x 6 faces of 256^2 to the k = 5 band, then the triple product
     of 1M vertices with separate BRDF and visibility (6 x 1024 coefficients each, qtree layout).
@@ -986,8 +981,8 @@ def run_triple(args, cfg):
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": e2e,
     }
     if not args.no_cpu_baseline:
-        full, desc = oracle_sample_triple(cfg, 4, 4000)
-        line["cpu_baseline"] = {"value": V / full, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+        t_s, rows_s, desc = oracle_sample(cfg, 256)
+        line["cpu_baseline"] = {"value": rows_s / t_s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
                                 "sample": desc}
     print(json.dumps(line), flush=True)
     return 0
@@ -1086,8 +1081,41 @@ def run_rotate(args, cfg):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(args) -> None:
+    """`--gpus N` is the number of ranks, one per GPU.  Under torchrun WORLD_SIZE must equal N;
+    without it (a plain `python bench.py --gpus N`) the script re-executes itself under
+    torch.distributed.run with N local ranks (rendezvous on 127.0.0.1) and exits with its status."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank per GPU",
+                  file=sys.stderr)
+            sys.exit(2)
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"[bench] --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}", file=sys.stderr)
+            sys.exit(2)
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse_args()
+    launch_ranks(args)
     cfg = synth.config(args.config)
     if args.vertices:
         cfg = synth.Config(**{**cfg.__dict__, "vertices": args.vertices})

@@ -12,7 +12,11 @@ One process per GPU (torchrun), torch.distributed over NCCL for the plumbing:
   - fused (``open_peer_view`` + ``relight_into_peer``, the default of bench.py): rank 0's radiance
     buffer is opened in every rank through CUDA IPC and each rank's relight kernel stores its
     rows straight into it over NVLink / NVSwitch from the epilogue -- the gather IS the relight's
-    output write, no separate collective, no staging copy;
+    output write, no separate collective, no staging copy; ``rows_landed_fence`` (a one-element
+    all-reduce on the stream) orders rank 0's later work after every rank's rows, stream-ordered;
+  - host buffers (``SharedHostBuffer`` + pipeline.ShardedShiftRelightPipeline): every rank copies
+    its own rows device->host into one shared page-locked host array, chunk by chunk under its
+    relight, so all N PCIe links carry the gather;
   - NCCL (``relight_and_gather``, the baseline and the fallback): chunk i is gathered on the NCCL
     stream while chunk i+1 is relit, so the gather overlaps the HBM-bound relight.
 
@@ -172,12 +176,71 @@ def open_peer_view(radiance_full: Optional[torch.Tensor], shape, device: torch.d
     return view
 
 
+def rows_landed_fence(flag: torch.Tensor, group=None) -> None:
+    """Stream-ordered completion of the fused relight + gather: a one-element all-reduce enqueued
+    on every rank's current stream after its relight.  It completes on rank 0 only once every
+    rank's relight kernel (whose epilogue stored into rank 0's buffer) has finished, so work that
+    rank 0 enqueues after it sees every row -- no host synchronisation, no host barrier.
+    ``flag``: a persistent one-element device tensor (int32)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(flag, group=group)
+
+
+class SharedHostBuffer:
+    """A float32 array in POSIX shared memory (/dev/shm) mapped by every rank of the node and
+    page-locked in each (cudaHostRegister), so that every rank's device->host copies land in one
+    host array over its own PCIe link: the N>1 radiance gather on the host side.  Rank 0 creates
+    the file, the others map it after a broadcast of its name; ``close`` unmaps and unpins (rank 0
+    unlinks)."""
+
+    def __init__(self, shape, group=None, pin: bool = True):
+        import mmap
+        import os
+        import numpy as np
+        self.shape = tuple(int(x) for x in shape)
+        self.nbytes = int(np.prod(self.shape)) * 4
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        name = [None]
+        if self.rank == 0:
+            name = [f"/dev/shm/hs_radiance_{os.getpid()}_{id(self)}"]
+            with open(name[0], "wb") as fh:
+                fh.truncate(self.nbytes)
+        if dist.is_initialized():
+            dist.broadcast_object_list(name, src=0, group=group)
+        self.path = name[0]
+        self._fh = open(self.path, "r+b")
+        self._mm = mmap.mmap(self._fh.fileno(), self.nbytes)
+        self.array = np.ndarray(self.shape, dtype=np.float32, buffer=self._mm)
+        self.tensor = torch.from_numpy(self.array)
+        self.pinned = False
+        if pin and torch.cuda.is_available():
+            err = torch.cuda.cudart().cudaHostRegister(self.tensor.data_ptr(), self.nbytes, 0)
+            if int(err) != 0:
+                raise RuntimeError(f"cudaHostRegister of the shared radiance buffer failed ({err})")
+            self.pinned = True
+
+    def close(self) -> None:
+        import os
+        if self.pinned:
+            torch.cuda.cudart().cudaHostUnregister(self.tensor.data_ptr())
+            self.pinned = False
+        self.tensor = None
+        self.array = None
+        self._mm.close()
+        self._fh.close()
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+        if self.rank == 0 and os.path.exists(self.path):
+            os.unlink(self.path)
+
+
 def relight_into_peer(transfer_local: torch.Tensor, band: torch.Tensor, total_rows: int,
                       relight_fn: Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None],
                       radiance_view: torch.Tensor, group=None) -> None:
     """The fused relight + gather: this rank's rows are written by the relight kernel directly at
     their global offset of rank 0's radiance (``radiance_view`` from ``open_peer_view``).  The
-    caller orders completion (stream synchronise + barrier) before rank 0 reads the buffer."""
+    caller orders completion (``rows_landed_fence``) before rank 0 reads the buffer."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     start, count = shard_rows(total_rows, world, rank)

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import api
-from .dist import chunk_bounds
+from .dist import allgather_band, chunk_bounds, shard_rows
 
 
 class ShiftRelightPipeline:
@@ -85,6 +85,97 @@ class ShiftRelightPipeline:
                 self.ev_copied[c].record(self.d2h)
         self.i += 1
         return self.ev_copied[-1]
+
+
+class ShardedShiftRelightPipeline:
+    """The host-buffer step at N > 1 ranks: per step, every rank copies only its own
+    frames' light pyramids host -> device, shifts them to the band (``haar_shift_coeffs``), the band
+    is all-gathered over NCCL / NVLink (``dist.allgather_band``, the one exchange step), and the
+    rank relights its own vertex rows chunk by chunk, each chunk's radiance copied device -> host
+    straight into the rank's rows of ``radiance_host`` -- a ``dist.SharedHostBuffer`` every rank
+    maps -- while the next chunk computes.  The host gather therefore runs over all N PCIe links
+    at once instead of funnelling the whole radiance through rank 0's.  Plumbing only; the compute
+    is the C-ABI kernels.  Single rank: the same schedule with a local band copy."""
+
+    def __init__(self, transfer_local: torch.Tensor, faces: int, log2n: int, batch: int, band_levels: int,
+                 total_rows: int, chunks: int = 4, group=None):
+        import torch.distributed as dist
+        dev = transfer_local.device
+        N = 1 << log2n
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        self.row0, count = shard_rows(total_rows, world, rank)
+        if transfer_local.shape[0] != count:
+            raise ValueError(f"rank {rank}: expected {count} transfer rows, got {transfer_local.shape[0]}")
+        self.f0, self.fn = shard_rows(batch, world, rank)
+        self.T = transfer_local
+        self.faces, self.log2n, self.batch, self.band = faces, log2n, batch, band_levels
+        self.k_face = 4 ** band_levels
+        self.light = [torch.empty((max(self.fn, 1), faces, N * N), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.band_local = torch.empty((max(self.fn, 1), faces, self.k_face), dtype=torch.float32, device=dev)
+        self.band_full = torch.empty((batch, faces, self.k_face), dtype=torch.float32, device=dev)
+        self.R = torch.empty((count, batch), dtype=torch.float32, device=dev)
+        self.ws = torch.empty(max(api.haar_shift_workspace_bytes(2, log2n, faces, max(self.fn, 1)), 1),
+                              dtype=torch.uint8, device=dev)
+        rws = api.relight_workspace_bytes(faces, self.k_face, batch)
+        self.rws = None
+        if rws:
+            raw = torch.empty(rws + 1024, dtype=torch.uint8, device=dev)
+            self.rws = raw[(-raw.data_ptr()) % 1024:]
+        self.chunks = chunk_bounds(count, chunks)
+        self.compute = torch.cuda.current_stream(dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        self.ev_light_free = [torch.cuda.Event() for _ in range(2)]
+        self.ev_chunk = [torch.cuda.Event() for _ in self.chunks]
+        self.ev_copied = [torch.cuda.Event() for _ in self.chunks]
+        self.ev_done = torch.cuda.Event()
+        self.i = 0
+        self.launches = 0
+
+    def h2d_bytes(self) -> int:
+        return self.fn * self.faces * (1 << (2 * self.log2n)) * 4
+
+    def d2h_bytes(self) -> int:
+        return self.R.numel() * 4
+
+    def step(self, light_host: torch.Tensor, shifts, radiance_host: torch.Tensor) -> torch.cuda.Event:
+        """light_host: pinned [batch][faces][N*N] (this rank copies its frames); shifts: host
+        [batch][faces][2]; radiance_host: the shared pinned [total_rows][batch] buffer.  Returns an
+        event that completes when this rank's rows are in radiance_host."""
+        buf = self.i & 1
+        f0, fn = self.f0, self.fn
+        if fn:
+            with torch.cuda.stream(self.h2d):
+                if self.i >= 2:
+                    self.h2d.wait_event(self.ev_light_free[buf])
+                self.light[buf][:fn].copy_(light_host[f0:f0 + fn], non_blocking=True)
+                self.ev_h2d[buf].record(self.h2d)
+            self.compute.wait_event(self.ev_h2d[buf])
+            sh = np.asarray(shifts, dtype=np.float64)[f0:f0 + fn]
+            api.haar_shift_coeffs(self.light[buf][:fn], sh, 2, self.band, out=self.band_local[:fn],
+                                  workspace=self.ws, stream=self.compute)
+            self.launches += api.last_launch_count()
+        self.ev_light_free[buf].record(self.compute)
+        with torch.cuda.stream(self.compute):
+            allgather_band(self.band_local[:fn], self.band_full, group=self.group)
+        for c, (s, n) in enumerate(self.chunks):
+            if self.i >= 1:
+                self.compute.wait_event(self.ev_copied[c])   # the previous step's D2H of this chunk is done
+            api.relight_vertices(self.T[s:s + n], self.band_full, self.faces, self.k_face, out=self.R[s:s + n],
+                                 workspace=self.rws, stream=self.compute)
+            self.launches += api.last_launch_count()
+            self.ev_chunk[c].record(self.compute)
+            self.d2h.wait_event(self.ev_chunk[c])
+            with torch.cuda.stream(self.d2h):
+                g = self.row0 + s
+                radiance_host[g:g + n].copy_(self.R[s:s + n], non_blocking=True)
+                self.ev_copied[c].record(self.d2h)
+        self.ev_done.record(self.d2h)
+        self.i += 1
+        return self.ev_done
 
 
 class ShiftTripleRelightPipeline(ShiftRelightPipeline):

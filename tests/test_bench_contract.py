@@ -38,3 +38,37 @@ def test_our_arm_line():
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_gpus_flag_launches_one_rank_per_gpu():
+    """`python bench.py --gpus 2` (no WORLD_SIZE) re-executes itself under torch.distributed.run
+    with 2 ranks; rank 0 alone prints the line (reference arm: runs on CPU) and reports 2 GPUs"""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_world_size_mismatch_is_an_error():
+    env = {**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
+
+
+def test_too_few_gpus_is_an_error():
+    try:
+        import torch
+        if torch.cuda.device_count() >= 64:
+            pytest.skip("enough GPUs")
+    except Exception:
+        pass
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "needs 64 GPUs" in out.stderr

@@ -133,3 +133,47 @@ def test_sharded_shift_band_allgather(world, B):
         msgs.append(q.get())
     assert all(p.exitcode == 0 for p in procs), msgs
     assert len([m for m in msgs if m[0] == "ok" and m[2]]) == world, msgs
+
+
+def _shared_worker(rank, world, port, V, B, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        buf = hsdist.SharedHostBuffer((V, B), pin=False)
+        s, c = hsdist.shard_rows(V, world, rank)
+        buf.tensor[s:s + c] = torch.arange(s * B, (s + c) * B, dtype=torch.float32).reshape(c, B)  # this rank's rows
+        flag = torch.zeros(1, dtype=torch.int32)
+        hsdist.rows_landed_fence(flag)          # gloo: a blocking all-reduce
+        dist.barrier()
+        if rank == 0:
+            want = torch.arange(V * B, dtype=torch.float32).reshape(V, B)
+            q.put(("ok", bool(torch.equal(buf.tensor, want))))
+        path = buf.path
+        buf.close()
+        if rank == 0:
+            q.put(("unlinked", not os.path.exists(path)))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), rank))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,V,B", [(2, 1001, 4), (3, 10, 64)])
+def test_shared_host_buffer_gathers_every_rank(world, V, B):
+    """the N>1 host gather: each rank writes its own rows into one /dev/shm array mapped by all
+    ranks; rank 0 sees every row; the file is removed on close"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shared_worker, args=(r, world, port, V, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    msgs = []
+    while not q.empty():
+        msgs.append(q.get())
+    assert all(p.exitcode == 0 for p in procs), msgs
+    assert ("ok", True) in msgs and ("unlinked", True) in msgs, msgs

@@ -134,3 +134,29 @@ def test_host_pipeline_matches_device_calls():
     torch.cuda.synchronize()
     for o, r in zip(outs, refs):
         assert torch.equal(o, r)
+
+
+def test_sharded_host_pipeline_single_rank_matches_device_calls():
+    """ShardedShiftRelightPipeline (the N>1 host-buffer step: own frames H2D, band shift, band
+    all-gather, chunked relight with per-chunk D2H into a shared page-locked host array), run as
+    one rank: bitwise the device calls' radiance, step after step"""
+    import torch
+    import paper_1705_07272_b200 as hs
+    from paper_1705_07272_b200 import dist as hsdist
+    from paper_1705_07272_b200.pipeline import ShardedShiftRelightPipeline
+    n, F, B, V, band = 5, 6, 64, 1000, 3
+    T = torch.empty((V, F * 4 ** band), dtype=torch.float32, device="cuda")
+    hs.hs_fill_transfer(T, 0, F, 4 ** band, 32, synth.STREAM_T)
+    pipe = ShardedShiftRelightPipeline(T, F, n, B, band, V, chunks=3)
+    shared = hsdist.SharedHostBuffer((V, B))
+    try:
+        for step in range(3):
+            light = synth.light_pyramids(50 + step, B, F, n)
+            sh = np.random.default_rng(10 + step).uniform(0, 32, size=(B, F, 2))
+            ev = pipe.step(torch.from_numpy(light).pin_memory(), sh, shared.tensor)
+            ev.synchronize()
+            s = hs.haar_shift_coeffs(torch.from_numpy(light).cuda(), sh, 2, band)
+            ref = hs.relight_vertices(T, s, F, 4 ** band).cpu()
+            assert torch.equal(shared.tensor, ref)
+    finally:
+        shared.close()
