@@ -67,7 +67,7 @@ def test_relight_sparse_shards_bitwise(B):
     F, n, ks, V = 6, 6, 64, 900
     idx = torch.empty((V, ks), dtype=torch.int32, device="cuda")
     val = torch.empty((V, ks), dtype=torch.float32, device="cuda")
-    hs.hs_fill_sparse_transfer(idx, val, 0, F, n, 2, 83)
+    hs.hs_fill_sparse_transfer(idx, val, 0, F, n, 1, 83)
     L = _dev(synth.light_pyramids(84, B, F, n))
     full = hs.relight_vertices_sparse(idx, val, L)
     for blocks in _blocks(V):
