@@ -137,16 +137,19 @@ HS_API size_t haar_shift_coarse_workspace_bytes(int in_log2n, int start_level, i
  *   workspace     device scratch of >= relight_workspace_bytes(faces, k_face, batch) bytes,
  *                 1024-byte aligned (may be NULL when that size is 0).
  * Accumulation is fp32.  batch <= 8: CUDA-core streaming GEMV.  batch a multiple of 64 with
- * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16.  Every 64-k
- * block of every transfer row is scaled by its own power of two 2^e (max |T| of the block ->
- * [2^14, 2^15)) and every light frame by its own power of two s_b before the fp16 hi + lo split;
- * three products per block accumulate in fp32 in TMEM, the epilogue drains each block into fp32
- * registers with the factor 2^-e and divides by s_b at the end.  Contract: ~2^-21 relative per
- * product for any finite fp32 transfer and light values (a block whose max |T| is below 2^-112,
- * i.e. outside fp32's normal range after the 2^-14 headroom, loses relative precision
- * gracefully); the result overflows only if sum |T L| * s_b / max|L_b s_b| does, i.e. when
- * |T| > ~2^100 together with K * 2^15 headroom.  Tested at T scaled by 2^-30 ... 2^60 and
- * with mixed row / block magnitudes (tests/test_gpu_range.py).  Other batches: CUDA-core tiled
+ * faces*k_face a multiple of 64: tcgen05 tensor-core GEMM in split-precision fp16.  Every light
+ * frame is scaled by a power of two s_b and every transfer row by a power of two 2^e picked from its
+ * first nonzero 64-k block (e = 0 when that block's max |T| is in [2^-4, 2^8), else the block's max
+ * is moved to [2^7, 2^8)); then x = hi + 2^-11 lo in fp16 pieces, three products per 64-k block
+ * accumulate in fp32 in TMEM, drained into fp32 registers every 1024 k, times 2^-e / s_b at the end.
+ * Contract: ~2^-21 relative per product for every value within 2^22 binades below the row's first
+ * nonzero block's max; a row with a later block more than 2^8 times larger than that (fp16
+ * overflow) comes out non-finite from the tensor cores, is listed by the kernel and recomputed
+ * exactly on the CUDA cores (fp64 accumulation, relight_redo_rows_kernel), so any finite fp32
+ * transfer and light values give a result accurate to ~1e-6 relative per row.  Each row's
+ * arithmetic depends on that row only (results are bitwise independent of row sharding).  Tested
+ * at T scaled by 2^-30 ... 2^60, 1e-30, and with mixed row / block / element magnitudes
+ * (tests/test_gpu_range.py).  Other batches: CUDA-core tiled
  * GEMM (fp32 FMA).
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status relight_vertices(const float* transfer, int64_t num_vertices, int faces, int k_face,
@@ -229,9 +232,9 @@ HS_API hs_status hs_fill_sparse_transfer(int32_t* indices, float* values, int64_
  *   workspace      >= relight_triple_workspace_bytes(...), 1024-byte aligned (HS_ERR_ALIGNMENT).
  *   Precision: fp32 inputs; the tripling terms are formed in fp32 and multiplied on the tensor
  *   cores in split fp16 (hi + 2^-11 lo) with fp32 accumulation when batch % 64 == 0 (DESIGN.md
- *   §5.8), each 64-term chunk of each row scaled by its own power of two first (as in
- *   relight_vertices: any fp32 magnitude of BRDF and visibility whose tripling terms stay
- *   finite), otherwise on CUDA cores in fp32.
+ *   §5.8), each row's terms scaled by a power of two first and rows that leave fp16's range
+ *   recomputed exactly on the CUDA cores, as in relight_vertices (any fp32 magnitude of BRDF and
+ *   visibility whose tripling terms stay finite), otherwise on CUDA cores in fp32.
  *
  * haar_pack_qtree -- HAAR1 -> qtree layout (the storage format of brdf_q / vis_q):
  *   in   DEVICE [rows][faces][in_face_stride] fp32, HAAR1 prefix of 4^log2k used per face;

@@ -124,8 +124,15 @@ struct ShiftArgs {
   long long in_face_stride;   // elements between the faces of one batch entry (>= K)
   long long ws_face_stride;   // BYTES per face in ws (ws_face_floats_2d doubles)
   int log2n, faces, band, out_face_stride, num_faces;
+  int stream;                 // 1: faces with kStreamMinLevel <= m <= kStreamMaxLevel go to shift2d_stream_kernel
   FaceParam fp[kMaxFacesPerLaunch];
 };
+
+// Working levels handled by the register-streaming shift kernel (shift2d_stream.cu).
+constexpr int kStreamMinLevel = 6;
+constexpr int kStreamMaxLevel = 8;
+inline __host__ __device__ bool stream_level(int m) { return m >= kStreamMinLevel && m <= kStreamMaxLevel; }
+hs_status launch_shift2d_stream(ShiftArgs& a, cudaStream_t st);   // shift2d_stream.cu
 
 // Tiling constants of the 2D tile kernel.
 constexpr int kTileKF = 3;    // fine levels per tile: the tile root level is c = max(0, m - KF)
@@ -158,6 +165,7 @@ constexpr int kTcLTileBytes = 16384;
 hs_status launch_relight_tc_prep(const float* L, long long lstride, int faces, int kface, int batch, void* ws,
                                  cudaStream_t st);
 bool relight_tc_eligible(int faces, int kface, int batch);
+size_t tc_redo_offset(int faces, int kface, int batch);   // RedoList (tc_ptx.cuh) inside the tc workspace
 hs_status launch_rowdot(const float* T, const float* S, long long rows, long long K, float* R,
                         cudaStream_t st);
 bool relight_shifted_fused_supported(int log2n);

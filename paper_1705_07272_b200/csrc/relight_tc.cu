@@ -1,27 +1,30 @@
 // Relight on the 5th-generation tensor cores (batch % 64 == 0):
 //   R[v][b] = sum_k T[v][k] L[b][k]        (double product, PAPER.md eq:tripleSum P:253-266)
-// in split-precision fp16 with fp32 accumulation in TMEM.  Per 64-k block kb of
-// row v, with e_vk a power-of-two exponent chosen from the block's own max |T| and s_b a per-frame
-// power of two chosen from max |L_b|:
-//   T 2^e = T_hi + 2^-11 T_lo,  L_b s_b = L_hi + 2^-11 L_lo   (fp16 pieces, max |.| in [2^14, 2^15))
-//   acc_hh = sum_kb T_hi L_hi,  acc_x = sum_kb (T_hi L_lo + T_lo L_hi)
-//   R = sum_kb 2^-e (acc_hh + 2^-11 acc_x) / s_b     (the dropped T_lo L_lo term is ~2^-22)
-// so the split is relative to each block's magnitude for any fp32 T (no fp16 overflow or
-// subnormal loss), and the tensor-core accumulation chain is one 64-k block long.
+// in split-precision fp16 with fp32 accumulation in TMEM.  With e_v a per-row
+// power of two picked by the converters (tc_ptx.cuh RowExp: 0 for transfer rows of ordinary
+// magnitude) and s_b a per-frame power of two chosen from max |L_b|:
+//   T 2^e = T_hi + 2^-11 T_lo,  L_b s_b = L_hi + 2^-11 L_lo   (fp16 pieces)
+//   acc_hh = sum T_hi L_hi,  acc_x = sum (T_hi L_lo + T_lo L_hi)
+//   R = 2^-e (acc_hh + 2^-11 acc_x) / s_b     (the dropped T_lo L_lo term is ~2^-22)
+// Rows whose split leaves fp16's range (non-finite result) are recomputed exactly by
+// relight_redo_rows_kernel, so the accuracy does not depend on the magnitude of T.
 //
 // Kernel anatomy (one CTA per SM, persistent over 128-row tiles, 12 warps):
 //   warp 0      TMA producer: T tile [128 rows x 64 k] fp32 (two 128B-swizzled boxes) + the
 //               pre-swizzled [L_hi | L_lo] band tile [128 x 64] fp16 (one bulk copy) per stage;
 //   warp 1      MMA issuer (one thread): per 16-k step, tcgen05.mma kind::f16 with A from TMEM:
 //                 D[acc_hh | acc_x] (N=128) += T_hi x [L_hi | L_lo];  D[acc_x] (N=64) += T_lo x L_hi
-//               into accumulator buffer (block count & 1), committed to the epilogue per block;
+//               into accumulator buffer (group count & 1); every KG = 16 k blocks it switches buffer
+//               and commits the finished group to the epilogue;
 //   warp 2      TMEM allocator (512 columns: 4 A stages x 64 + 2 accumulator buffers x 128);
-//   warps 4-7   converters: read their row of the T tile from smem, pick e_vk from the row's 64
-//               values, split T 2^e -> fp16 hi/lo and tcgen05.st them into the A stage (lane = row)
-//               -- T never round-trips through HBM; e_vk goes to the epilogue through an int8 ring;
-//   warps 8-11  epilogue: per k block, tcgen05.ld both accumulators of the finished buffer and add
-//               2^-e (acc_hh + 2^-11 acc_x) into fp32 registers; at the end of the tile scale by
-//               1/s_b and store the R rows.  The two buffers keep the drains off the MMA's path.
+//   warps 4-7   converters: read their row of the T tile from smem, split T 2^e -> fp16 hi/lo and
+//               tcgen05.st them into the A stage (lane = row) -- T never round-trips through HBM;
+//               the row exponent goes to the epilogue through an int8 ring per tile;
+//   warps 8-11  epilogue: drains each finished group (tcgen05.ld both accumulators, combine) into
+//               fp32 registers -- the tensor-core accumulation loses precision linearly in the
+//               chain length (3.1e-5 at K = 24576 as one chain, 2.0e-6 drained every 1024 k) and
+//               the two buffers keep the drains off the MMA's path -- then scales by 2^-e / s_b,
+//               stores the R rows and lists the non-finite ones for the exact redo.
 // All hand-offs are mbarriers; tcgen05.commit signals MMA completion.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -42,6 +45,7 @@ constexpr int BK = 64;            // k per stage
 constexpr int BN = 64;            // frames per block (MMA N of each accumulator)
 constexpr int STAGES = 4;         // smem stages
 constexpr int ASTAGES = 4;        // TMEM A stages
+constexpr int KG = 16;            // k-blocks per accumulation group, drained by the epilogue into fp32 registers
 constexpr int T_STAGE = BM * BK * 4;         // 32 KB
 constexpr int L_STAGE = 2 * BN * BK * 2;     // 16 KB: [L_hi 64 rows | L_lo 64 rows] x 128 B
 constexpr int SMEM_TILES = STAGES * (T_STAGE + L_STAGE);
@@ -57,8 +61,9 @@ constexpr uint32_t ACC_COL0 = ASTAGES * 64;  // 256
 // per (frame block, k block) -- exactly the 128B-swizzled K-major smem image the MMA reads.
 __global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __restrict__ L, long long lstride,
                                                                int faces, int kshift, int K, uint8_t* __restrict__ tiles,
-                                                               float* __restrict__ inv_scale) {
+                                                               float* __restrict__ inv_scale, RedoList* __restrict__ redo) {
   const int b = blockIdx.x;
+  if (b == 0 && threadIdx.x == 0) redo->count = 0;   // the main kernel lists its non-finite rows here
   const int fb = b / BN, r = b % BN;
   const int kmask = (1 << kshift) - 1;
   const float* Lb = L + (long long)b * faces * lstride;
@@ -100,10 +105,36 @@ __global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __res
 }
 
 // ------------------------------------------------------------------------------- main kernel
+// One converter thread: its row of the 128 x 64 fp32 T tile (two 128B-swizzled 32-k boxes) ->
+// fp16 hi / lo pieces of T 2^e in the TMEM A stage at taddr (hi columns 0..31, lo 32..63).
+template <bool SCALED>
+__device__ __forceinline__ void convert_block(const uint8_t* tb, int row, float sc, uint32_t taddr) {
+#pragma unroll
+  for (int box = 0; box < 2; ++box) {
+    const uint8_t* rowp = tb + box * (T_STAGE / 2);
+    float4 x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const float4*>(rowp + ((c ^ (row & 7)) << 4));
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (SCALED) {
+        split_pair_scaled(x[c].x, x[c].y, sc, hi[2 * c], lo[2 * c]);
+        split_pair_scaled(x[c].z, x[c].w, sc, hi[2 * c + 1], lo[2 * c + 1]);
+      } else {
+        split_pair(x[c].x, x[c].y, hi[2 * c], lo[2 * c]);
+        split_pair(x[c].z, x[c].w, hi[2 * c + 1], lo[2 * c + 1]);
+      }
+    }
+    tmem_st16(taddr + box * 16, hi);
+    tmem_st16(taddr + 32 + box * 16, lo);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     relight_tc_kernel(const __grid_constant__ CUtensorMap tmapT, const uint8_t* __restrict__ ltiles,
                       const float* __restrict__ inv_scale_g, float* __restrict__ R, long long V, int K, int B,
-                      int ntiles) {
+                      int ntiles, RedoList* __restrict__ redo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sT = smem;                                  // STAGES x 32 KB
@@ -177,12 +208,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0, astage = 0;
       uint32_t phase = 0, aphase = 0;
-      int gi = 0;   // k-block counter: accumulator buffer gi & 1
+      int gi = 0;   // accumulation group (KG k-blocks) counter: buffer gi & 1
       const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
       for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb, ++gi) {
+        for (int kb = 0; kb < nkb; ++kb) {
           const int acc = gi & 1;
-          mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
+          const bool first = (kb % KG) == 0;
+          if (first) {
+            mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
+            fence_after();
+          }
           const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
           mbar_wait(&full[stage], phase);
           mbar_wait(&afull[astage], aphase);
@@ -192,12 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bd = sw128_desc(lbase + kk * 32);
             const uint32_t ahi = tmem + astage * 64 + kk * 8;
-            tc_mma_ts(dhh, ahi, bd, id128, kk ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) T_hi x [L_hi | L_lo]
-            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);     // acc_x += T_lo x L_hi
+            tc_mma_ts(dhh, ahi, bd, id128, (!first || kk) ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) T_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);                  // acc_x += T_lo x L_hi
           }
           tc_commit(&empty[stage]);
           tc_commit(&aempty[astage]);
-          tc_commit(&tfull[acc]);   // block complete: the epilogue drains it into registers
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -205,6 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++astage == ASTAGES) {
             astage = 0;
             aphase ^= 1;
+          }
+          if ((kb % KG) == KG - 1 || kb == nkb - 1) {
+            tc_commit(&tfull[acc]);   // group complete: the epilogue drains it into registers
+            ++gi;
           }
         }
       }
@@ -216,36 +254,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     int stage = 0, astage = 0;
     uint32_t phase = 0, aphase = 0;
-    int gi = 0;
-    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb, ++gi) {
+    int tc = 0;   // tiles converted by this CTA: exponent ring slot tc & 7
+    RowExp rx;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++tc) {
+      for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         mbar_wait(&aempty[astage], aphase ^ 1);
         fence_after();
         const uint8_t* tb = sT + stage * T_STAGE + row * 128;
-        float4 v[16];
-        float mx = 0.f;
+        rx.update(kb, [&] {
+          float mx = 0.f;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          v[c] = *reinterpret_cast<const float4*>(tb + (c >> 3) * (T_STAGE / 2) + (((c & 7) ^ (row & 7)) << 4));
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w))));
-        }
-        const int e = split_exponent(mx);
-        const float sc = pow2i(e);
-        const int slot = gi & (kExpRing - 1);
-        sexp[slot * BM + row] = (int8_t)e;
-        mbar_arrive(&efull[slot]);
-#pragma unroll
-        for (int box = 0; box < 2; ++box) {
-          uint32_t hi[16], lo[16];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 x = v[box * 8 + c];
-            split_pair(x.x, x.y, sc, hi[2 * c], lo[2 * c]);
-            split_pair(x.z, x.w, sc, hi[2 * c + 1], lo[2 * c + 1]);
+          for (int c = 0; c < 16; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(tb + (c >> 3) * (T_STAGE / 2) + (((c & 7) ^ (row & 7)) << 4));
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
           }
-          tmem_st16(lane_base + astage * 64 + box * 16, hi);
-          tmem_st16(lane_base + astage * 64 + 32 + box * 16, lo);
+          return mx;
+        });
+        if (rx.scaled)   // warp-uniform: the whole block on one path, loads hoisted ahead of the splits
+          convert_block<true>(tb, row, pow2i(rx.e), lane_base + astage * 64);
+        else
+          convert_block<false>(tb, row, 1.f, lane_base + astage * 64);
+        if (kb == nkb - 1) {   // the row's exponent for this tile -> epilogue
+          sexp[(tc & (kExpRing - 1)) * BM + row] = (int8_t)rx.e;
+          mbar_arrive(&efull[tc & (kExpRing - 1)]);
         }
         tmem_wait_st();
         fence_before();
@@ -266,17 +298,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = threadIdx.x - 256;
     const int q = warp & 3;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    int gi = 0;
-    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+    int gi = 0, tc = 0;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++tc) {
       const int tile = (int)(w / nfb), fb = (int)(w % nfb);
       const long long grow = (long long)tile * BM + row;
       float sum[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-      for (int kb = 0; kb < nkb; ++kb, ++gi) {
-        const int slot = gi & (kExpRing - 1);
-        mbar_wait(&efull[slot], (gi / kExpRing) & 1);
-        const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row's block
+      for (int g0 = 0; g0 < nkb; g0 += KG, ++gi) {
         const int acc = gi & 1;
         mbar_wait(&tfull[acc], (gi >> 1) & 1);
         fence_after();
@@ -287,22 +316,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] = fmaf(fmaf(xx[j], 1.f / 2048.f, hh[j]), rs, sum[c * 16 + j]);
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += fmaf(xx[j], 1.f / 2048.f, hh[j]);
         }
         fence_before();
         mbar_arrive(&tempty[acc]);
       }
+      const int slot = tc & (kExpRing - 1);
+      mbar_wait(&efull[slot], (tc / kExpRing) & 1);
+      const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row
       if (grow < V) {
         float* out = R + grow * B + fb * BN;
+        bool bad = false;
 #pragma unroll
         for (int j = 0; j < BN; j += 4) {
           float4 o;
-          o.x = sum[j + 0] * __ldg(inv_scale_g + fb * BN + j + 0);
-          o.y = sum[j + 1] * __ldg(inv_scale_g + fb * BN + j + 1);
-          o.z = sum[j + 2] * __ldg(inv_scale_g + fb * BN + j + 2);
-          o.w = sum[j + 3] * __ldg(inv_scale_g + fb * BN + j + 3);
+          o.x = sum[j + 0] * rs * __ldg(inv_scale_g + fb * BN + j + 0);
+          o.y = sum[j + 1] * rs * __ldg(inv_scale_g + fb * BN + j + 1);
+          o.z = sum[j + 2] * rs * __ldg(inv_scale_g + fb * BN + j + 2);
+          o.w = sum[j + 3] * rs * __ldg(inv_scale_g + fb * BN + j + 3);
+          bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
           *reinterpret_cast<float4*>(out + j) = o;
         }
+        if (bad) redo_push(redo, grow);   // recomputed exactly by relight_redo_rows_kernel
       }
     }
   }
@@ -316,6 +351,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+// Workspace: light tiles [batch/64][K/64] x 16 KB | inv_scale [batch] fp32 | RedoList (256-aligned).
+size_t tc_tiles_bytes(int faces, int kface, int batch) {
+  return (size_t)(batch / BN) * (size_t)((long long)faces * kface / BK) * L_STAGE;
+}
+size_t tc_redo_offset(int faces, int kface, int batch) {
+  return (tc_tiles_bytes(faces, kface, batch) + (size_t)batch * sizeof(float) + 255) & ~size_t(255);
+}
+
+struct PlainRow {   // the transfer row itself
+  const float* T;
+  long long K;
+  __device__ void operator()(long long row, int k0, int nk, float* sx) const {
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) sx[i] = __ldg(T + row * K + k0 + i);
+  }
+};
+
 bool relight_tc_eligible(int faces, int kface, int batch) {
   const long long K = (long long)faces * kface;
   return batch % BN == 0 && K % BK == 0 && K >= BK;
@@ -323,8 +374,7 @@ bool relight_tc_eligible(int faces, int kface, int batch) {
 
 size_t relight_tc_workspace_bytes(int faces, int kface, int batch) {
   if (!relight_tc_eligible(faces, kface, batch)) return 0;
-  const long long K = (long long)faces * kface;
-  return (size_t)(batch / BN) * (size_t)(K / BK) * L_STAGE + (size_t)batch * sizeof(float) + 256;
+  return tc_redo_offset(faces, kface, batch) + sizeof(RedoList);
 }
 
 hs_status launch_relight_tc_prep(const float* L, long long lstride, int faces, int kface, int batch, void* ws,
@@ -333,8 +383,9 @@ hs_status launch_relight_tc_prep(const float* L, long long lstride, int faces, i
   int kshift = 0;
   while ((1 << kshift) < kface) ++kshift;
   uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
-  float* inv = reinterpret_cast<float*>(tiles + (size_t)(batch / BN) * (size_t)(K / BK) * L_STAGE);
-  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv);
+  float* inv = reinterpret_cast<float*>(tiles + tc_tiles_bytes(faces, kface, batch));
+  RedoList* redo = reinterpret_cast<RedoList*>(tiles + tc_redo_offset(faces, kface, batch));
+  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);
   HS_CHECK_LAUNCH("relight_tc_prep_kernel");
   return HS_OK;
 }
@@ -351,7 +402,8 @@ hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, c
   int kshift = 0;
   while ((1 << kshift) < kface) ++kshift;
   uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
-  float* inv = reinterpret_cast<float*>(tiles + (size_t)(batch / BN) * (size_t)(K / BK) * L_STAGE);
+  float* inv = reinterpret_cast<float*>(tiles + tc_tiles_bytes(faces, kface, batch));
+  RedoList* redo = reinterpret_cast<RedoList*>(tiles + tc_redo_offset(faces, kface, batch));
 
   CUtensorMap map;
   const cuuint64_t gdim[2] = {(cuuint64_t)K, (cuuint64_t)V};
@@ -367,13 +419,16 @@ hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, c
   }
   HS_SMEM_ATTR(relight_tc_kernel, SMEM_BYTES);
 
-  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv);
+  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);
   HS_CHECK_LAUNCH("relight_tc_prep_kernel");
   const int ntiles = (int)((V + BM - 1) / BM);
   const long long nwork = (long long)ntiles * (batch / BN);
   const int grid = (int)(nwork < num_sms() ? nwork : num_sms());
-  relight_tc_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(map, tiles, inv, R, V, K, batch, ntiles);
+  relight_tc_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(map, tiles, inv, R, V, K, batch, ntiles, redo);
   HS_CHECK_LAUNCH("relight_tc_kernel");
+  relight_redo_rows_kernel<PlainRow><<<num_sms(), 128, 0, st>>>(PlainRow{T, K}, L, (long long)faces * lstride, lstride,
+                                                               kshift, K, batch, R, V, redo);
+  HS_CHECK_LAUNCH("relight_redo_rows_kernel");
   *handled = true;
   return HS_OK;
 }

@@ -31,10 +31,11 @@
 //     warp 1  MMA issuer (tcgen05.mma kind::f16, A from TMEM) -- as in relight_tc.cu
 //     warp 2  TMEM allocator
 //     warps 4-7  converters: evaluate the tripling terms of their row's chunk from smem, scale
-//                them by 2^e (max |M| of the chunk in [2^14, 2^15)), split fp32 -> fp16 hi/lo,
+//                them by the row's power of two 2^e (tc_ptx.cuh RowExp), split fp32 -> fp16 hi/lo,
 //                tcgen05.st into the A stage -- M never touches HBM
-//     warps 8-11 epilogue: drains every k block into fp32 registers with the converters'
-//                per-(row, block) power-of-two scale, then the per-frame scale, as in relight_tc.cu
+//     warps 8-11 epilogue: drains every KG = 16 k blocks into fp32 registers, scales by 2^-e and
+//                the per-frame scale, lists non-finite rows for the exact CUDA-core redo
+//                (relight_redo_rows_kernel), as in relight_tc.cu
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -190,6 +191,7 @@ constexpr int BM = 128, BK = 64, BN = 64;
 constexpr int DSTAGES = 3;                      // rho + V tiles
 constexpr int LSTAGES = 2;                      // light tiles
 constexpr int ASTAGES = 4;                      // TMEM A stages
+constexpr int KG = 16;                          // k blocks per accumulation group (relight_tc.cu)
 constexpr int T_TILE = BM * BK * 4;             // 32 KB per operand tile
 constexpr int D_STAGE = 2 * T_TILE;             // rho | V
 constexpr int L_STAGE = kTcLTileBytes;          // 16 KB
@@ -204,7 +206,8 @@ static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 __global__ void __launch_bounds__(kThreads, 1)
     relight_triple_tc_kernel(const __grid_constant__ CUtensorMap tmapR, const __grid_constant__ CUtensorMap tmapV,
                              const uint8_t* __restrict__ ltiles, const float* __restrict__ inv_scale_g,
-                             float* __restrict__ R, long long V, int K, int B, int ntiles, float w0, float inv_cells) {
+                             float* __restrict__ R, long long V, int K, int B, int ntiles, float w0, float inv_cells,
+                             RedoList* __restrict__ redo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sD = smem;                                   // DSTAGES x (rho 32 KB | V 32 KB)
@@ -305,12 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int lstage = 0, astage = 0;
       uint32_t lphase = 0, aphase = 0;
-      int gi = 0;   // k-block counter: accumulator buffer gi & 1
+      int gi = 0;   // accumulation group counter: buffer gi & 1
       const uint32_t id128 = idesc_f16(2 * BN), id64 = idesc_f16(BN);
       for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb, ++gi) {
+        for (int kb = 0; kb < nkb; ++kb) {
           const int acc = gi & 1;
-          mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
+          const bool first = (kb % KG) == 0;
+          if (first) {
+            mbar_wait(&tempty[acc], ((gi >> 1) & 1) ^ 1);   // the epilogue drained this buffer
+            fence_after();
+          }
           const uint32_t dhh = tmem + ACC_COL0 + acc * 128;
           mbar_wait(&lfull[lstage], lphase);
           mbar_wait(&afull[astage], aphase);
@@ -320,12 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t bd = sw128_desc(lbase + kk * 32);
             const uint32_t ahi = tmem + astage * 64 + kk * 8;
-            tc_mma_ts(dhh, ahi, bd, id128, kk ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) M_hi x [L_hi | L_lo]
-            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);     // acc_x += M_lo x L_hi
+            tc_mma_ts(dhh, ahi, bd, id128, (!first || kk) ? 1u : 0u);   // [acc_hh | acc_x] (=|+=) M_hi x [L_hi | L_lo]
+            tc_mma_ts(dhh + BN, ahi + 32, bd, id64, 1u);                  // acc_x += M_lo x L_hi
           }
           tc_commit(&lempty[lstage]);
           tc_commit(&aempty[astage]);
-          tc_commit(&tfull[acc]);   // block complete: the epilogue drains it into registers
           if (++lstage == LSTAGES) {
             lstage = 0;
             lphase ^= 1;
@@ -333,6 +339,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++astage == ASTAGES) {
             astage = 0;
             aphase ^= 1;
+          }
+          if ((kb % KG) == KG - 1 || kb == nkb - 1) {
+            tc_commit(&tfull[acc]);
+            ++gi;
           }
         }
       }
@@ -345,9 +355,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sw = row & 7;
     int stage = 0, astage = 0;
     uint32_t phase = 0, aphase = 0;
-    int gi = 0;
-    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb, ++gi) {
+    int tc = 0;   // tiles converted by this CTA: exponent ring slot tc & 7
+    RowExp rx;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++tc) {
+      for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&dfull[stage], phase);
         mbar_wait(&aempty[astage], aphase ^ 1);
         fence_after();
@@ -358,21 +369,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             [&](int u) { return *reinterpret_cast<const float4*>(tr + (u >> 3) * (T_TILE / 2) + (((u & 7) ^ sw) << 4)); },
             [&](int u) { return *reinterpret_cast<const float4*>(tv + (u >> 3) * (T_TILE / 2) + (((u & 7) ^ sw) << 4)); },
             w0, inv_cells, o);
-        float mx = 0.f;
+        rx.update(kb, [&] {
+          float mx = 0.f;
 #pragma unroll
-        for (int i = 0; i < QC; ++i) mx = fmaxf(mx, fabsf(o[i]));
-        const int e = split_exponent(mx);
-        const float sc = pow2i(e);
-        const int slot = gi & (kExpRing - 1);
-        sexp[slot * BM + row] = (int8_t)e;
-        mbar_arrive(&efull[slot]);
+          for (int i = 0; i < QC; ++i) mx = fmaxf(mx, fabsf(o[i]));
+          return mx;
+        });
+        const float sc = pow2i(rx.e);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t hi[16], lo[16];
+          if (rx.scaled) {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) split_pair(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], sc, hi[c], lo[c]);
+            for (int c = 0; c < 16; ++c) split_pair_scaled(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], sc, hi[c], lo[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) split_pair(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], hi[c], lo[c]);
+          }
           tmem_st16(lane_base + astage * 64 + h * 16, hi);
           tmem_st16(lane_base + astage * 64 + 32 + h * 16, lo);
+        }
+        if (kb == nkb - 1) {
+          sexp[(tc & (kExpRing - 1)) * BM + row] = (int8_t)rx.e;
+          mbar_arrive(&efull[tc & (kExpRing - 1)]);
         }
         tmem_wait_st();
         fence_before();
@@ -393,17 +412,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = threadIdx.x - 256;
     const int q = warp & 3;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    int gi = 0;
-    for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
+    int gi = 0, tc = 0;
+    for (long long w = blockIdx.x; w < nwork; w += gridDim.x, ++tc) {
       const int tile = (int)(w / nfb), fb = (int)(w % nfb);
       const long long grow = (long long)tile * BM + row;
       float sum[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-      for (int kb = 0; kb < nkb; ++kb, ++gi) {
-        const int slot = gi & (kExpRing - 1);
-        mbar_wait(&efull[slot], (gi / kExpRing) & 1);
-        const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row's block
+      for (int g0 = 0; g0 < nkb; g0 += KG, ++gi) {
         const int acc = gi & 1;
         mbar_wait(&tfull[acc], (gi >> 1) & 1);
         fence_after();
@@ -414,22 +430,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld16(lane_base + ACC_COL0 + acc * 128 + BN + c * 16, xx);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] = fmaf(fmaf(xx[j], 1.f / 2048.f, hh[j]), rs, sum[c * 16 + j]);
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += fmaf(xx[j], 1.f / 2048.f, hh[j]);
         }
         fence_before();
         mbar_arrive(&tempty[acc]);
       }
+      const int slot = tc & (kExpRing - 1);
+      mbar_wait(&efull[slot], (tc / kExpRing) & 1);
+      const float rs = pow2i(-(int)sexp[slot * BM + row]);   // 2^-e of this row
       if (grow < V) {
         float* out = R + grow * B + fb * BN;
+        bool bad = false;
 #pragma unroll
         for (int j = 0; j < BN; j += 4) {
           float4 o;
-          o.x = sum[j + 0] * __ldg(inv_scale_g + fb * BN + j + 0);
-          o.y = sum[j + 1] * __ldg(inv_scale_g + fb * BN + j + 1);
-          o.z = sum[j + 2] * __ldg(inv_scale_g + fb * BN + j + 2);
-          o.w = sum[j + 3] * __ldg(inv_scale_g + fb * BN + j + 3);
+          o.x = sum[j + 0] * rs * __ldg(inv_scale_g + fb * BN + j + 0);
+          o.y = sum[j + 1] * rs * __ldg(inv_scale_g + fb * BN + j + 1);
+          o.z = sum[j + 2] * rs * __ldg(inv_scale_g + fb * BN + j + 2);
+          o.w = sum[j + 3] * rs * __ldg(inv_scale_g + fb * BN + j + 3);
+          bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
           *reinterpret_cast<float4*>(out + j) = o;
         }
+        if (bad) redo_push(redo, grow);
       }
     }
   }
@@ -450,6 +472,21 @@ int log2_of(long long x) {
 }
 
 bool triple_tc_eligible(int faces, int kface, int batch) { return relight_tc_eligible(faces, kface, batch); }
+
+struct TripleRow {   // the tripling terms of a row, chunk by chunk (relight_redo_rows_kernel)
+  const float* rq;
+  const float* vq;
+  long long K;
+  float w0, inv_cells;
+  __device__ void operator()(long long row, int k0, int nk, float* sx) const {
+    for (int c = threadIdx.x; c < nk / QC; c += blockDim.x) {
+      const float4* pr = reinterpret_cast<const float4*>(rq + row * K + k0 + (long long)c * QC);
+      const float4* pv = reinterpret_cast<const float4*>(vq + row * K + k0 + (long long)c * QC);
+      triple_chunk([&](int u) { return __ldg(pr + u); }, [&](int u) { return __ldg(pv + u); }, w0, inv_cells,
+                   sx + c * QC);
+    }
+  }
+};
 
 }  // namespace
 
@@ -513,9 +550,13 @@ hs_status launch_relight_triple(const float* brdf_q, const float* vis_q, long lo
     const int ntiles = (int)((V + BM - 1) / BM);
     const long long nwork = (long long)ntiles * (batch / BN);
     const int grid = (int)(nwork < num_sms() ? nwork : num_sms());
+    RedoList* redo = reinterpret_cast<RedoList*>(rest + tc_redo_offset(faces, kface, batch));
     relight_triple_tc_kernel<<<grid, kThreads, SMEM_BYTES, st>>>(maps[0], maps[1], rest, inv, R, V, (int)K, batch,
-                                                                 ntiles, w0, inv_cells);
+                                                                 ntiles, w0, inv_cells, redo);
     HS_CHECK_LAUNCH("relight_triple_tc_kernel");
+    relight_redo_rows_kernel<TripleRow><<<num_sms(), 128, 0, st>>>(TripleRow{brdf_q, vis_q, K, w0, inv_cells}, lq, K,
+                                                                  kface, k * 2, (int)K, batch, R, V, redo);
+    HS_CHECK_LAUNCH("relight_redo_rows_kernel");
     return HS_OK;
   }
 

@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(FT) == 4 ? 3 : 2) shift2d_til
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int m = P.m;
   if (m == 0) return;  // identity: handled by permute_kernel
+  if (args.stream && stream_level(m)) return;   // shift2d_stream_kernel
   const int c = m > KF ? m - KF : 0;
   const int k = m - c;
   const int tc = (1 << c) < TC ? (1 << c) : TC;
@@ -735,7 +736,7 @@ __global__ void permute_kernel(const __grid_constant__ ShiftArgs args) {
 }
 
 template <typename FT>
-hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_t st) {
+hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_tile, bool any_stream, cudaStream_t st) {
   HS_SMEM_ATTR(shift2d_tile_kernel<FT>, max_tile_smem<FT>());
   HS_SMEM_ATTR(coarse_fields_kernel, kFieldsSmem);
   HS_SMEM_ATTR(coarse_finish_kernel<FT>, kFinishSmem);
@@ -743,8 +744,14 @@ hs_status launch_tiles(ShiftArgs& a, int max_tiles, bool any_coarse, cudaStream_
     coarse_fields_kernel<<<a.num_faces, kThreads, kFieldsSmem, st>>>(a);
     HS_CHECK_LAUNCH("coarse_fields_kernel");
   }
-  shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);
-  HS_CHECK_LAUNCH("shift2d_tile_kernel");
+  if (any_tile) {
+    shift2d_tile_kernel<FT><<<dim3(max_tiles, a.num_faces), kThreads, max_tile_smem<FT>(), st>>>(a);
+    HS_CHECK_LAUNCH("shift2d_tile_kernel");
+  }
+  if (any_stream) {
+    hs_status s = launch_shift2d_stream(a, st);
+    if (s != HS_OK) return s;
+  }
   if (any_coarse) {
     coarse_finish_kernel<FT><<<a.num_faces, kThreads, kFinishSmem, st>>>(a);
     HS_CHECK_LAUNCH("coarse_finish_kernel");
@@ -862,7 +869,8 @@ __global__ void __launch_bounds__(kThreads) shift2d_small_kernel(const __grid_co
 
 }  // namespace
 
-hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, cudaStream_t st) {
+hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, bool any_tile, bool any_stream,
+                         cudaStream_t st) {
   if (a.log2n <= kSmallMaxLog2n) {
     const size_t smem = (size_t)(1 << (2 * a.log2n)) * 4 +
                         ((size_t)3 * (1 << (2 * a.log2n)) * 2 + 3 * (1 << (2 * (a.log2n > 0 ? a.log2n - 1 : 0)))) * 8;
@@ -875,7 +883,7 @@ hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_
     // fp64 fields at every size: fp32 rounding in the difference fields is amplified ~2^(n-l) on a
     // band of level l; the randomised sweep (tests/test_gpu_fuzz.py) measured
     // 2e-5 for white noise at N = 64 with fp32 fields.
-    hs_status s = launch_tiles<double>(a, max_tiles, any_coarse, st);
+    hs_status s = launch_tiles<double>(a, max_tiles, any_coarse, any_tile, any_stream && a.stream, st);
     if (s != HS_OK) return s;
   }
   if (any_perm) {

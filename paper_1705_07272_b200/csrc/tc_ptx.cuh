@@ -130,32 +130,140 @@ __device__ __forceinline__ float2 resid2048(float2 v, float2 h) {
 
 
 // ------------------------------------------------------------------------------- range handling
-// Per-(row, 64-k block) power-of-two exponents of the split-precision tensor-core relights
-// (DESIGN.md §5.3): the converter thread that owns a row scales the block's values by 2^e so that
-// their max |x| lands in [2^14, 2^15) -- the top of fp16's range -- before the hi/lo split, and
-// passes e to the epilogue through a ring of kExpRing int8 slots per row; the epilogue drains the
-// block's accumulators and multiplies them by 2^-e.  The split is then relative to the block's own
-// magnitude for every fp32 input, not just |x| in fp16's range.
+// Per-row power-of-two exponents of the split-precision tensor-core relights.
+// The converter thread that owns a row picks e_v from the row's FIRST NONZERO 64-k block (in the
+// common case block 0: one max over 64 values per row and tile) and splits every block of the row
+// as x 2^e_v = hi + 2^-11 lo.  e_v = 0 while that block's max |x| lies in [2^-4, 2^8) -- then no
+// scaling instruction runs at all -- else the scaled max lands in [2^7, 2^8).  Either way the split
+// of every value is relative to the value itself for the 2^22 binades below the block's max, and
+// the other blocks of the row may be up to 2^8 times larger before x 2^e_v leaves fp16's range.
+// A row that does (|x 2^e_v| >= 65520: fp16 overflow) ends with a non-finite accumulator; the
+// epilogue lists it and relight_redo_rows_kernel recomputes it exactly on the CUDA cores (fp64
+// accumulation).  Every row's arithmetic depends on its own data only, so results do not depend on
+// which rows share a tile (sharding is bitwise exact).  The epilogue multiplies by 2^-e_v, passed
+// per (tile, row) through a ring of kExpRing int8 slots.
 constexpr int kExpRing = 8;
-__device__ __forceinline__ int split_exponent(float mx) {
-  if (!(mx > 0.f) || !isfinite(mx)) return 0;   // zero block: any e; inf / NaN propagate unscaled
-  const int e = 14 - ilogbf(mx);
+__device__ __forceinline__ int row_exponent(float mx) {   // mx > 0, finite
+  const int ex = ilogbf(mx);
+  if (ex >= -4 && ex <= 7) return 0;
+  const int e = 7 - ex;
   return e < -126 ? -126 : (e > 126 ? 126 : e);
 }
 __device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }   // e in [-126, 127]
-// fp16 hi / lo pieces of (a, b) * sc (sc a power of two: exact), lo = (x - hi) 2^11
-__device__ __forceinline__ void split_pair(float a, float b, float sc, uint32_t& hi, uint32_t& lo) {
+// fp16 hi / lo pieces of (a, b), lo = (x - hi) 2^11
+__device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const float2 r = resid2048(make_float2(a, b), hf);
+  const __half2 l = __floats2half2_rn(r.x, r.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// the same for (a, b) * sc (sc a power of two: the scaling is exact)
+__device__ __forceinline__ void split_pair_scaled(float a, float b, float sc, uint32_t& hi, uint32_t& lo) {
   float2 v;
   asm("{\n\t.reg .b64 va, k;\n\tmov.b64 va, {%2, %3};\n\tmov.b64 k, {%4, %4};\n\t"
       "mul.rn.f32x2 va, va, k;\n\tmov.b64 {%0, %1}, va;\n\t}"
       : "=f"(v.x), "=f"(v.y)
       : "f"(a), "f"(b), "f"(sc));
-  const __half2 h = __floats2half2_rn(v.x, v.y);
-  const float2 hf = __half22float2(h);
-  const float2 r = resid2048(v, hf);
-  const __half2 l = __floats2half2_rn(r.x, r.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
+  split_pair(v.x, v.y, hi, lo);
+}
+// Converter-side row exponent state: call at every k block (uniform control flow per warp).
+struct RowExp {
+  int e = 0;
+  bool set = false, all_set = false, scaled = false;
+  // kb == 0 resets; while any row of the warp is unset, `block_max()` is evaluated (warp-uniform).
+  template <class MAXF>
+  __device__ __forceinline__ void update(int kb, MAXF block_max) {
+    if (kb == 0) {
+      set = false;
+      all_set = false;
+      e = 0;
+    }
+    if (!all_set) {
+      const float mx = block_max();
+      if (!set && mx > 0.f && isfinite(mx)) {   // zero / non-finite blocks leave the row unset
+        e = row_exponent(mx);
+        set = true;
+      }
+      all_set = __all_sync(0xffffffffu, set);
+      scaled = __any_sync(0xffffffffu, e != 0);
+    }
+  }
+};
+// Rows whose result came out non-finite (epilogue -> relight_redo_rows_kernel), in the workspace.
+constexpr int kRedoCap = 8192;
+struct RedoList {
+  int count;
+  int pad[3];
+  long long rows[kRedoCap];
+};
+__device__ __forceinline__ void redo_push(RedoList* rl, long long row) {
+  const int i = atomicAdd(&rl->count, 1);
+  if (i < kRedoCap) rl->rows[i] = row;
+}
+
+// Exact recomputation of the listed rows on the CUDA cores: R[v][b] = sum_k x_v[k] L[b][k] with
+// fp64 accumulation, x_v produced in shared-memory chunks by `fill` (the transfer row itself, or the
+// tripling terms of relight_triple.cu).  L[b][k] = L[b * lbstride + (k >> kshift) * lstride +
+// (k & (2^kshift - 1))].  One CTA of 128 threads per row; if more rows than kRedoCap were listed,
+// every row whose radiance holds a non-finite value is recomputed instead (a scan of R).
+constexpr int kRedoChunk = 2048;
+template <class FILL>
+__global__ void __launch_bounds__(128) relight_redo_rows_kernel(FILL fill, const float* __restrict__ L,
+                                                                long long lbstride, long long lstride, int kshift,
+                                                                int K, int B, float* __restrict__ R, long long V,
+                                                                const RedoList* __restrict__ rl) {
+  __shared__ float sx[kRedoChunk];
+  __shared__ int sbad;
+  const int cnt = rl->count;
+  if (cnt == 0) return;
+  const bool scan = cnt > kRedoCap;
+  const long long n = scan ? V : cnt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long kmask = (1ll << kshift) - 1;
+  for (long long e = blockIdx.x; e < n; e += gridDim.x) {
+    const long long row = scan ? e : rl->rows[e];
+    if (scan) {
+      if (threadIdx.x == 0) sbad = 0;
+      __syncthreads();
+      for (int b = threadIdx.x; b < B; b += blockDim.x)
+        if (!isfinite(R[row * B + b])) sbad = 1;
+      __syncthreads();
+      const int bad = sbad;
+      __syncthreads();
+      if (!bad) continue;
+    }
+    for (int fb0 = 0; fb0 < B; fb0 += 64) {
+      double acc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += kRedoChunk) {
+        const int nk = (K - k0) < kRedoChunk ? (K - k0) : kRedoChunk;
+        __syncthreads();
+        fill(row, k0, nk, sx);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int b = fb0 + warp * 16 + i;
+          const float* Lb = L + (long long)b * lbstride;
+          double a = acc[i];
+          for (int k = lane; k < nk; k += 32) {
+            const long long kk = k0 + k;
+            a = fma((double)sx[k], (double)__ldg(Lb + (kk >> kshift) * lstride + (kk & kmask)), a);
+          }
+          acc[i] = a;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        double a = acc[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) R[row * B + fb0 + warp * 16 + i] = (float)a;
+      }
+    }
+  }
 }
 
 }  // namespace tc
