@@ -11,11 +11,12 @@
 // outputs are then four rolled reads of precomputed planes instead of a shift + stencil:
 //   planes_kernel   (per face and field, fp64): D1[4][64][64] (level n-1 details), D2[16][32][32]
 //                   (level n-2 details), F2[16][32][32] (level n-2 fields), scales folded in;
-//   planes3_kernel  DF3[64][16][16] (level n-3 (detail, field) pairs) from F2;
+//   planes3_kernel  D3[64][16][16] and F3 (level n-3 details and fields) from F2;
+//   planes_low_kernel DL: the details of levels n-4 .. 0, 4^n values per level (residues x cells);
 //   planes_a_kernel one warp per vertex: sum_ab w_ab (< T_{n-1}, roll(D1_ab) > + < T_{n-2}, roll(D2_ab) >)
 //                   (D1 rows doubled in shared memory so a warp's 64 rows never wrap; HBM-bound);
-//   planes_c_kernel one warp per vertex: level n-3 details and field from DF3 the same way, then the
-//                   bottom-up 3 .. 0 warp-synchronously (T: 1.4 KB);
+//   planes_c_kernel one warp per vertex: levels n-3 .. 0 the same way (D3 in shared memory, DL gathered
+//                   from L2 one vertex ahead with the T values) -- no per-vertex bottom-up;
 //   finish          r_v = the 2 x 3F partials + sum_f T_v[f][0] L_f[0].
 // No block barriers after the plane fills: every warp owns its vertex.
 #include <cuda_runtime.h>
@@ -28,8 +29,10 @@ constexpr int kPN = 7;                    // log2 N of this path
 constexpr int kPG = 64;                   // level n-1 side
 constexpr int kPD1 = 4 * kPG * kPG;       // D1 floats
 constexpr int kPD2 = 16 * 32 * 32;        // D2 (and F2) floats
-constexpr int kPD3 = 2 * 64 * 16 * 16;    // level n-3 (detail, field) pairs, 64 residues
-constexpr int kPlanesPerUnit = kPD1 + 2 * kPD2 + kPD3;
+constexpr int kPD3 = 2 * 64 * 16 * 16;    // level n-3 details D3[64][256], then fields F3[64][256]
+constexpr int kPL = 1 << (2 * kPN);       // one residue-plane level below n-3: 4^k residues x 4^(n-k) cells
+constexpr int kPDL = 4 * kPL;             // details of levels n-4 .. 0 (k = 4 .. 7)
+constexpr int kPlanesPerUnit = kPD1 + 2 * kPD2 + kPD3 + kPDL;
 
 namespace {
 
@@ -98,13 +101,14 @@ __global__ void __launch_bounds__(512) planes_kernel(const double* __restrict__ 
 // level n-3, residues rho'' in {0..7}^2:  P_{3,rho''} = BU(roll(P_{2, rho'' mod 4}, rho'' div 4)), from
 // the (fp32) level n-2 fields F2 of planes_kernel
 template <int FLD>
-__device__ void planes3_body(const float* F2, float2* DF3) {
+__device__ void planes3_body(const float* F2, float* D3, float* F3) {
   for (int idx = threadIdx.x; idx < 64 * 256; idx += blockDim.x) {
     const int rho = idx >> 8, cell = idx & 255, i = cell >> 4, j = cell & 15;
     const int ry = rho >> 3, rx = rho & 7;
     float fv, dv;
     bu_rolled<float, FLD>(F2 + (((ry & 3) << 2) | (rx & 3)) * 1024, 32, i, j, ry >> 2, rx >> 2, fv, dv);
-    DF3[idx] = make_float2(dv * pw2(-(kPN - 3)), fv);
+    D3[idx] = dv * pw2(-(kPN - 3));
+    F3[idx] = fv;
   }
 }
 
@@ -112,10 +116,50 @@ __global__ void __launch_bounds__(256) planes3_kernel(float* __restrict__ planes
   const int t = blockIdx.x % 3;
   float* base = planes + (long long)blockIdx.x * kPlanesPerUnit;
   const float* F2 = base + kPD1 + kPD2;
-  float2* DF3 = reinterpret_cast<float2*>(base + kPD1 + 2 * kPD2);
-  if (t == 0) planes3_body<0>(F2, DF3);
-  else if (t == 1) planes3_body<1>(F2, DF3);
-  else planes3_body<2>(F2, DF3);
+  float* D3 = base + kPD1 + 2 * kPD2;
+  if (t == 0) planes3_body<0>(F2, D3, D3 + kPD3 / 2);
+  else if (t == 1) planes3_body<1>(F2, D3, D3 + kPD3 / 2);
+  else planes3_body<2>(F2, D3, D3 + kPD3 / 2);
+}
+
+// levels n-4 .. 0 (k = 4 .. 7): P_{k,rho} = BU(roll(P_{k-1, rho mod 2^(k-1)}, rho div 2^(k-1))) over
+// the 4^k residues rho, each a 2^(n-k) square: 4^n values per level, ping-ponged in shared memory
+// (fields) from F3; the details (scaled to unit-square) go to DL[k - 4].
+template <int FLD>
+__device__ void planes_low_body(const float* __restrict__ F3, float* __restrict__ DL, float* Fa, float* Fb) {
+  for (int idx = threadIdx.x; idx < kPL; idx += blockDim.x) Fa[idx] = F3[idx];
+  __syncthreads();
+  const float* src = Fa;
+  float* dst = Fb;
+#pragma unroll 1
+  for (int k = 4; k <= kPN; ++k) {
+    const int l = kPN - k, side = 1 << l, rk = 1 << k, rh = rk >> 1;   // cells side^2, residues rk^2
+    for (int idx = threadIdx.x; idx < kPL; idx += blockDim.x) {
+      const int rho = idx >> (2 * l), cell = idx & (side * side - 1);
+      const int ry = rho >> k, rx = rho & (rk - 1);
+      const int i = cell >> l, j = cell & (side - 1);
+      const int parent = ((ry & (rh - 1)) << (k - 1)) | (rx & (rh - 1));
+      float fv, dv;
+      bu_rolled<float, FLD>(src + parent * (4 * side * side), 2 * side, i, j, ry >> (k - 1), rx >> (k - 1), fv, dv);
+      DL[(k - 4) * kPL + idx] = dv * pw2(-l);
+      dst[idx] = fv;
+    }
+    __syncthreads();
+    const float* t = src;
+    src = dst;
+    dst = const_cast<float*>(t);
+  }
+}
+
+__global__ void __launch_bounds__(512) planes_low_kernel(float* __restrict__ planes) {
+  extern __shared__ float smL[];   // two field ping-pong buffers of kPL floats
+  const int t = blockIdx.x % 3;
+  float* base = planes + (long long)blockIdx.x * kPlanesPerUnit;
+  const float* F3 = base + kPD1 + 2 * kPD2 + kPD3 / 2;
+  float* DL = base + kPD1 + 2 * kPD2 + kPD3;
+  if (t == 0) planes_low_body<0>(F3, DL, smL, smL + kPL);
+  else if (t == 1) planes_low_body<1>(F3, DL, smL, smL + kPL);
+  else planes_low_body<2>(F3, DL, smL, smL + kPL);
 }
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -213,113 +257,133 @@ __global__ void __launch_bounds__(kAWarps * 32, 1)
 }
 
 // ------------------------------------------------------------------------------- level n-3 .. 0
-constexpr int kCWarps = 32;
-constexpr int kCScr = 256 + 64 + 16 + 4;   // per warp: level n-3, 3, 2, 1 planes
-constexpr int kCSmem = (kPD3 + kCWarps * kCScr) * 4;
+// Levels n-3 .. 0 of one unit per vertex: four rolled reads of the residue planes per output cell
+// (level n-3 from shared memory, levels n-4 .. 0 from the L2-resident DL), no bottom-up.  The T
+// values and the DL gathers of the next vertex are in flight while the current one is reduced.
+constexpr int kCWarps = 16;
+constexpr int kCSmem = kPD3 * 4;   // D3[64][32][16]: rows doubled so a lane's 8 rows never wrap
 
-template <int FLD>
-__device__ __forceinline__ float planes_c_vertex(const float2* DF3s, float* S3, const float* __restrict__ Tv, int4 pr,
-                                                 int lane) {
-  // T values of levels n-3 .. 0 of this type, requested first
-  float t3[8];
+struct CTvals {
+  float t3[8];      // level n-3 T: cells lane + 32 k
+  float t4[2];      // level n-4 T: cells lane, lane + 32
+  float tl[3];      // levels 2, 1, 0 (n = 7) T: cell lane & 15 / lane & 3 / 0, zero on duplicate lanes
+  float g4[2][4];   // level n-4 plane values per cell and combo (a, b)
+  float gl[3][4];   // levels 2, 1, 0 plane values per combo
+  int4 pr;
+};
+// plane value of level L (k = kPN - L) cell (i, j) for combo Q = (qy, qx): residue (Q mod 2^k), roll
+// Q div 2^k (the residue / roll part is the same for every lane of the warp)
+template <int L>
+__device__ __forceinline__ float low_gather(const float* __restrict__ DL, int qy, int qx, int i, int j) {
+  constexpr int k = kPN - L, side = 1 << L;
+  const int rho = ((qy & ((1 << k) - 1)) << k) | (qx & ((1 << k) - 1));
+  return __ldg(DL + (k - 4) * kPL + rho * side * side + (((i - (qy >> k)) & (side - 1)) << L) +
+               ((j - (qx >> k)) & (side - 1)));
+}
+__device__ __forceinline__ void planes_c_load(CTvals& c, const float* __restrict__ Tv, int fld,
+                                              const int4* __restrict__ vp, const float* __restrict__ DL, int lane) {
+  c.pr = __ldg(vp);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) t3[k] = __ldg(Tv + (1 + FLD) * 256 + lane + 32 * k);
-  const float t4a = __ldg(Tv + (1 + FLD) * 64 + lane), t4b = __ldg(Tv + (1 + FLD) * 64 + 32 + lane);
-  const float t5 = lane < 16 ? __ldg(Tv + (1 + FLD) * 16 + lane) : 0.f;
-  const float t6 = lane < 4 ? __ldg(Tv + (1 + FLD) * 4 + lane) : 0.f;
-  const float t7 = lane < 1 ? __ldg(Tv + (1 + FLD)) : 0.f;
+  for (int k = 0; k < 8; ++k) c.t3[k] = __ldg(Tv + (1 + fld) * 256 + lane + 32 * k);
+  c.t4[0] = __ldg(Tv + (1 + fld) * 64 + lane);
+  c.t4[1] = __ldg(Tv + (1 + fld) * 64 + 32 + lane);
+  const int c2 = lane & 15, c1 = lane & 3;
+  c.tl[0] = __ldg(Tv + (1 + fld) * 16 + c2);
+  c.tl[1] = __ldg(Tv + (1 + fld) * 4 + c1);
+  c.tl[2] = __ldg(Tv + (1 + fld));
+  if (lane >= 16) c.tl[0] = 0.f;   // each cell counted by one lane
+  if (lane >= 4) c.tl[1] = 0.f;
+  if (lane >= 1) c.tl[2] = 0.f;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int qy = (c.pr.x + a) & 127, qx = (c.pr.y + b) & 127;
+      c.g4[0][2 * a + b] = low_gather<3>(DL, qy, qx, lane >> 3, lane & 7);
+      c.g4[1][2 * a + b] = low_gather<3>(DL, qy, qx, (lane >> 3) + 4, lane & 7);
+      c.gl[0][2 * a + b] = low_gather<2>(DL, qy, qx, c2 >> 2, c2 & 3);
+      c.gl[1][2 * a + b] = low_gather<1>(DL, qy, qx, c1 >> 1, c1 & 1);
+      c.gl[2][2 * a + b] = low_gather<0>(DL, qy, qx, 0, 0);
+    }
+}
+
+__device__ __forceinline__ float planes_c_vertex(uint32_t d3base, const CTvals& cv, int lane) {
+  const int4 pr = cv.pr;
   const float wy1 = __int_as_float(pr.z), wx1 = __int_as_float(pr.w), wy0 = 1.f - wy1, wx0 = 1.f - wx1;
-  const float w[2][2] = {{wy0 * wx0, wy0 * wx1}, {wy1 * wx0, wy1 * wx1}};
-  // combo (a, b): Q = q + (a, b); residue Q & 7, roll Q >> 3.  Cell lane + 32 k = (row 2k + lane / 16,
-  // column lane % 16): a half-warp reads one rolled 16-wide row
+  const float w[4] = {wy0 * wx0, wy0 * wx1, wy1 * wx0, wy1 * wx1};
+  // level n-3: cell lane + 32 k = (row 2k + lane / 16, column lane % 16), combo residue Q & 7, roll
+  // Q >> 3: a half-warp reads one rolled 16-wide row; with the doubled rows, row 2k + rs_a of the
+  // residue plane is an immediate offset (128 k bytes) from the combo's base
   const int jl = lane & 15, il = lane >> 4;
-  int off[2][2], ry[2];
+  uint32_t ad[2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
-    ry[a] = ((pr.x + a) & 127) >> 3;
+    const int qy = (pr.x + a) & 127;
+    const int rs = (il - (qy >> 3)) & 15;
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
-      off[a][b] = ((((pr.x + a) & 7) << 3) | ((pr.y + b) & 7)) * 256 + ((jl - (((pr.y + b) & 127) >> 3)) & 15);
+    for (int b = 0; b < 2; ++b) {
+      const int qx = (pr.y + b) & 127;
+      const int rho = ((qy & 7) << 3) | (qx & 7);
+      ad[a][b] = d3base + (uint32_t)(((rho * 32 + rs) * 16 + ((jl - (qx >> 3)) & 15)) * 4);
+    }
   }
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int i = 2 * k + il;
-    float d = 0.f, fv = 0.f;
+    float d = 0.f;
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int row = ((i - ry[a]) & 15) * 16;
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const float2 p = DF3s[off[a][b] + row];
-        d = fmaf(w[a][b], p.x, d);
-        fv = fmaf(w[a][b], p.y, fv);
-      }
-    }
-    S3[lane + 32 * k] = fv;
-    acc = fmaf(d, t3[k], acc);
+      for (int b = 0; b < 2; ++b) d = fmaf(w[2 * a + b], lds(ad[a][b] + 128 * k), d);
+    acc = fmaf(d, cv.t3[k], acc);
   }
-  __syncwarp();
-  float* W3 = S3 + 256;
-  float* W2 = W3 + 64;
-  float* W1 = W2 + 16;
+  // levels n-4 .. 0 from the gathered plane values
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int idx = lane + 32 * k;
-    float f2, dv;
-    bu_rolled<float, FLD>(S3, 16, idx >> 3, idx & 7, 0, 0, f2, dv);
-    W3[idx] = f2;
-    acc = fmaf(dv * pw2(-3), k ? t4b : t4a, acc);
+  for (int h = 0; h < 2; ++h) {
+    float d = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d = fmaf(w[c], cv.g4[h][c], d);
+    acc = fmaf(d, cv.t4[h], acc);
   }
-  __syncwarp();
-  if (lane < 16) {
-    float f2, dv;
-    bu_rolled<float, FLD>(W3, 8, lane >> 2, lane & 3, 0, 0, f2, dv);
-    W2[lane] = f2;
-    acc = fmaf(dv * pw2(-2), t5, acc);
-  }
-  __syncwarp();
-  if (lane < 4) {
-    float f2, dv;
-    bu_rolled<float, FLD>(W2, 4, lane >> 1, lane & 1, 0, 0, f2, dv);
-    W1[lane] = f2;
-    acc = fmaf(dv * pw2(-1), t6, acc);
-  }
-  __syncwarp();
-  if (lane == 0) {
-    float f2, dv;
-    bu_rolled<float, FLD>(W1, 2, 0, 0, 0, 0, f2, dv);
-    acc = fmaf(dv, t7, acc);
+#pragma unroll
+  for (int h = 0; h < 3; ++h) {
+    float d = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d = fmaf(w[c], cv.gl[h][c], d);
+    acc = fmaf(d, cv.tl[h], acc);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  __syncwarp();   // S3 .. W1 are rewritten by this warp's next vertex
   return acc;
 }
 
 __global__ void __launch_bounds__(kCWarps * 32, 1)
     planes_c_kernel(const float* __restrict__ T, long long V, int faces, const float* __restrict__ planes,
                     const int4* __restrict__ vparams, float* __restrict__ partial, int nsplit) {
-  extern __shared__ __align__(16) float smC[];
-  const float2* DF3s = reinterpret_cast<const float2*>(smC);
+  extern __shared__ __align__(16) float D3s[];
   const int units = 3 * faces;
   const int unit = blockIdx.x % units, split = blockIdx.x / units;
   const int f = unit / 3, t = unit - 3 * (unit / 3);
   const float* src = planes + (long long)unit * kPlanesPerUnit + kPD1 + 2 * kPD2;
-  for (int idx = threadIdx.x; idx < kPD3; idx += blockDim.x) smC[idx] = __ldg(src + idx);
+  const float* DL = src + kPD3;
+  for (int idx = threadIdx.x; idx < kPD3; idx += blockDim.x) {   // [rho][row 0..31][col] <- [rho][row & 15][col]
+    const int rho = idx >> 9, r = (idx >> 4) & 31, c = idx & 15;
+    D3s[idx] = __ldg(src + rho * 256 + (r & 15) * 16 + c);
+  }
   __syncthreads();
+  const uint32_t d3base = saddr(D3s);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* S3 = smC + kPD3 + warp * kCScr;
   const long long NN = 1ll << (2 * kPN);
   const long long Kt = (long long)faces * NN;
   const long long v0 = V * split / nsplit, v1 = V * (split + 1) / nsplit;
+  // software pipeline: the next vertex's T values, parameters and plane gathers are in flight
+  CTvals cur, nxt;
+  if (v0 + warp < v1) planes_c_load(nxt, T + (v0 + warp) * Kt + (long long)f * NN, t, vparams + v0 + warp, DL, lane);
   for (long long v = v0 + warp; v < v1; v += kCWarps) {
-    const int4 pr = __ldg(vparams + v);
-    const float* Tv = T + v * Kt + (long long)f * NN;
-    float r;
-    if (t == 0) r = planes_c_vertex<0>(DF3s, S3, Tv, pr, lane);
-    else if (t == 1) r = planes_c_vertex<1>(DF3s, S3, Tv, pr, lane);
-    else r = planes_c_vertex<2>(DF3s, S3, Tv, pr, lane);
+    cur = nxt;
+    if (v + kCWarps < v1)
+      planes_c_load(nxt, T + (v + kCWarps) * Kt + (long long)f * NN, t, vparams + v + kCWarps, DL, lane);
+    const float r = planes_c_vertex(d3base, cur, lane);
     if (lane == 0) partial[v * 2 * units + units + unit] = r;
   }
 }
@@ -527,6 +591,9 @@ hs_status launch_relight_planes(const float* T, long long V, int faces, const fl
   HS_CHECK_LAUNCH("planes_kernel");
   planes3_kernel<<<units, 256, 0, st>>>(planes);
   HS_CHECK_LAUNCH("planes3_kernel");
+  HS_SMEM_ATTR(planes_low_kernel, 2 * kPL * 4);
+  planes_low_kernel<<<units, 512, 2 * kPL * 4, st>>>(planes);
+  HS_CHECK_LAUNCH("planes_low_kernel");
   int nsplit = sm_count() / units;
   if (nsplit < 1) nsplit = 1;
   if (nsplit > V) nsplit = (int)V;
