@@ -1113,6 +1113,124 @@ def launch_ranks(args) -> None:
     sys.exit(subprocess.call(cmd))
 
 
+def run_shade(args, cfg):
+    """c7s (rows f1 + f3, the paper's shading): shift 64 light frames (lat-long
+    N x N) to the band, then relight_vertices_brdf_rotated -- one BRDF rotated per vertex normal in
+    the Haar domain, triple product with the vertex's visibility.  One GPU."""
+    import torch
+
+    import paper_1705_07272_b200 as hs
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    V = args.vertices or cfg.vertices
+    n, B, k, kf = cfg.log2n, cfg.frames, cfg.band_levels, cfg.k_face
+    N = 1 << n
+    brdf = torch.from_numpy(synth.smooth_sphere_maps(cfg.seed, 1, n)[0]).to(dev)
+    vis_np = synth.shading_rows(cfg.seed, 0, V, 1, kf, synth.STREAM_VIS)
+    vq = hs.haar_pack_qtree(torch.from_numpy(vis_np).to(dev).view(V, 1, kf), k).view(V, kf)
+    rng = np.random.default_rng([cfg.seed, 7])
+    nv = rng.normal(size=(V, 3))
+    nv /= np.linalg.norm(nv, axis=1, keepdims=True)
+    normals = np.stack([np.arccos(np.clip(nv[:, 1], -1.0, 1.0)), np.mod(np.arctan2(nv[:, 0], nv[:, 2]), 2 * np.pi)], 1)
+    light_np = synth.light_pyramids(cfg.seed, B, 1, n)
+    light = torch.from_numpy(light_np).to(dev)
+    shifts = np.stack([np.zeros(B), np.arange(B) * N / 64.0], axis=1)[:, None, :]   # azimuth steps (global shift)
+    band = torch.empty((B, 1, kf), dtype=torch.float32, device=dev)
+    sws = torch.empty(hs.haar_shift_workspace_bytes(2, n, 1, B), dtype=torch.uint8, device=dev)
+    need = hs.relight_brdf_rotated_workspace_bytes(n, k, B)
+    wraw = torch.empty(need + 1024, dtype=torch.uint8, device=dev)
+    ws = wraw[(-wraw.data_ptr()) % 1024:]
+    R = torch.empty((V, B), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = {"n": 0}
+
+    def step():
+        hs.haar_shift_coeffs(light, shifts, 2, k, out=band, workspace=sws)
+        launches["n"] += hs.last_launch_count()
+        hs.relight_vertices_brdf_rotated(brdf, normals, vq, band.view(B, kf), k, out=R, workspace=ws)
+        launches["n"] += hs.last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches["n"] = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        time.sleep(0.01)
+        clk.mark(True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        clk.mark(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    peak, peak_src = hbm_peak()
+    NN = N * N
+    # algorithmic HBM bytes of the composed call: the rotated BRDF pyramids written and read back
+    # (4 B x N^2 each way), the qtree bands (4 B x kf each way), visibility 4 B x kf, radiance 4 B x B
+    alg = V * (NN * 8 + kf * 12 + B * 4) + B * kf * 4
+    e2e = None
+    if not args.no_e2e:
+        light_h = torch.from_numpy(light_np).pin_memory()
+        Rh = torch.empty((V, B), dtype=torch.float32).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            light.copy_(light_h, non_blocking=True)
+            step()
+            Rh.copy_(R, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            light.copy_(light_h, non_blocking=True)
+            step()
+            Rh.copy_(R, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / args.steps
+        e2e = {"value": V / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(light_np.nbytes),
+               "d2h_bytes_per_step": int(V * B * 4), "ms_per_step": e_ms,
+               "note": "pinned H2D of the 64 light pyramids, shift, composed rotate + triple call, pinned D2H of R; "
+                       "BRDF, normals and visibility are scene data"}
+    line = {
+        "metric": METRIC, "value": V / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.note}", "faces": 1, "N": N, "frames": B, "vertices": V,
+                   "k_face": kf, "l2": "no flush"},
+        "roofline": {"bound": "alu", "kernel": "relight_vertices_brdf_rotated (rotation + pack + triple product)",
+                     "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None, "alg_bytes_per_launch": alg,
+                     "avg_launch_ms": ms, "share_of_step": 1.0,
+                     "note": "reported against HBM for scale; the per-vertex rotation's fp64 chain rule (acos / "
+                             "atan2 per rotated sample) bounds the call, as in c6r"},
+        "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import relight as orelight
+        from oracle import rotate as orot
+        rows = 24
+        t0 = time.perf_counter()
+        band_np = np.stack([synth_shift_band(light_np[b, 0], shifts[b, 0], k) for b in range(B)])
+        rho = np.stack([orot.rotate_coeffs_chain(synth.smooth_sphere_maps(cfg.seed, 1, n)[0].astype(np.float64),
+                                                 float(normals[v, 0]), float(normals[v, 1]))[:kf]
+                        for v in range(rows)])
+        orelight.relight_triple(rho, vis_np[:rows].astype(np.float64), band_np[:, None, :], 1, kf)
+        t_s = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": rows / t_s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                                "sample": f"oracle fp64 on {rows} of {V} vertices (measured): the 64 frames' shift, "
+                                          f"{rows} chain-rule rotations of the BRDF, the triple integral"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def synth_shift_band(pyr, shift2, k):
+    """oracle shift of one lat-long pyramid, band prefix (CPU baseline of c7s)"""
+    from oracle import shift as oshift
+    return oshift.shift_coeffs(pyr[None, None, :].astype(np.float64), np.asarray(shift2)[None, None, :], 2)[0, 0, :4 ** k]
+
+
 def main():
     args = parse_args()
     launch_ranks(args)
@@ -1129,6 +1247,8 @@ def main():
         return run_triple(args, cfg)
     if cfg.name == "c6r":
         return run_rotate(args, cfg)
+    if cfg.name == "c7s":
+        return run_shade(args, cfg)
     return run_ours(args, cfg)
 
 

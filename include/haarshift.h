@@ -257,6 +257,36 @@ HS_API hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64
                                  float* out, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * relight_vertices_brdf_rotated -- the paper's shading composed (SURVEY.md §8(f) f1 + f3):
+ *   R[v][b] = integral over the lat-long map of  L_b * Rot(theta_v, phi_v) rho * V_v,
+ * band-limited to the HAAR1 prefix of 4^log2k coefficients, where rho is ONE BRDF map in the local
+ * frame of the surface (pole = normal) rotated per vertex by its normal's elevation and azimuth
+ * ("rotate the BRDF by the normal's angles, then the triple
+ * integral"; R28) -- haar_rotate_coeffs(rho, (alpha, beta) = (theta_v, phi_v)), then
+ * haar_pack_qtree, then relight_vertices_triple, chunked over 4096 vertices, all on the device.
+ *   brdf          DEVICE [N*N] fp32 HAAR1 pyramid of the local-frame BRDF (N = 2^log2n, lat-long:
+ *                 rows theta in [0, pi] top first, columns phi in [0, 2 pi)).
+ *   normals_host  HOST [num_vertices][2] fp64 (theta_N, phi_N) radians.
+ *   vis_q         DEVICE [num_vertices][4^log2k] fp32 visibility bands in the qtree layout
+ *                 (haar_pack_qtree of their HAAR1 prefixes).
+ *   light         DEVICE [batch][light_stride] fp32: each frame's HAAR1 prefix of >= 4^log2k
+ *                 entries (a full pyramid, stride N*N, or a band, stride 4^log2k); stride % 4 == 0.
+ *   radiance      DEVICE [num_vertices][batch] fp32 (16-byte aligned when batch % 64 == 0).
+ *   log2n 3 .. 11, log2k 3 .. log2n, batch 1 .. 1024; workspace >= relight_brdf_rotated_workspace_bytes,
+ *   1024-byte aligned.
+ *   Accuracy: the triple product as relight_vertices_triple; the rotation is the paper's first-order
+ *   chain rule (haar_rotate_coeffs), so against the spatial rotation the radiance is approximate
+ *   (PSNR, rising with N).
+ * ------------------------------------------------------------------------------------------- */
+HS_API hs_status relight_vertices_brdf_rotated(const float* brdf, int log2n, const double* normals_host,
+                                               int64_t num_vertices, const float* vis_q, int log2k,
+                                               const float* light, int64_t light_stride, int batch,
+                                               float* radiance, void* workspace, size_t workspace_bytes,
+                                               void* stream);
+
+HS_API size_t relight_brdf_rotated_workspace_bytes(int log2n, int log2k, int batch);
+
+/* ---------------------------------------------------------------------------------------------
  * haar_rotate_coeffs -- rotation of lat-long maps directly on their Haar coefficients (SURVEY.md
  * §8(f) f1; the paper's "non-linear phase shift").
  *

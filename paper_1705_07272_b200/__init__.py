@@ -12,6 +12,8 @@ device memory and streams.  Function names follow the C ABI:
   ``haar_pack_qtree`` converts HAAR1 pyramids to its qtree storage layout
 * ``haar_shift_coeffs_coarse`` coarse-start shift (f4)
 * ``haar_rotate_coeffs``       rotation of lat-long maps in the Haar domain (f1)
+* ``relight_vertices_brdf_rotated``  the paper's shading: BRDF rotated per vertex normal (f1), then
+  the triple product with light and visibility (f3)
 * ``hs_fill_transfer``         seeded synthetic transfer rows generated in place (input generator)
 
 See DESIGN.md for the method, its readings of the paper, layouts and kernels.
@@ -39,6 +41,8 @@ from .api import (  # noqa: F401
     relight_vertices_sparse,
     relight_triple_workspace_bytes,
     relight_vertices_triple,
+    relight_brdf_rotated_workspace_bytes,
+    relight_vertices_brdf_rotated,
     shift_and_relight,
 )
 
@@ -48,4 +52,5 @@ __all__ = [
     "shift_and_relight", "hs_fill_sparse_transfer", "relight_vertices_sparse",
     "relight_sparse_workspace_bytes", "haar_pack_qtree", "relight_triple_workspace_bytes", "relight_vertices_triple",
     "haar_rotate_coeffs", "haar_rotate_workspace_bytes", "enable_peer_access",
+    "relight_vertices_brdf_rotated", "relight_brdf_rotated_workspace_bytes",
 ]

@@ -37,6 +37,10 @@ SIGNATURES = {
     "relight_triple_workspace_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int, _c.c_int, _c.c_int]),
     "haar_pack_qtree": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int, _c.c_int64, _c.c_int, _c.c_void_p,
                                    _c.c_void_p]),
+    "relight_vertices_brdf_rotated": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int,
+                                                 _c.c_void_p, _c.c_int64, _c.c_int, _c.c_void_p, _c.c_void_p,
+                                                 _c.c_size_t, _c.c_void_p]),
+    "relight_brdf_rotated_workspace_bytes": (_c.c_size_t, [_c.c_int, _c.c_int, _c.c_int]),
     "haar_rotate_coeffs": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p,
                                       _c.c_size_t, _c.c_void_p]),
     "haar_rotate_workspace_bytes": (_c.c_size_t, [_c.c_int, _c.c_int]),

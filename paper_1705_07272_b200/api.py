@@ -285,6 +285,42 @@ def relight_vertices_triple(brdf_q: torch.Tensor, vis_q: torch.Tensor, light: to
     return out
 
 
+def relight_brdf_rotated_workspace_bytes(log2n: int, log2k: int, batch: int) -> int:
+    return int(load().relight_brdf_rotated_workspace_bytes(log2n, log2k, batch))
+
+
+def relight_vertices_brdf_rotated(brdf: torch.Tensor, normals, vis_q: torch.Tensor, light: torch.Tensor, log2k: int,
+                                  out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """brdf [N*N] (local-frame lat-long BRDF, HAAR1), normals host [V][2] fp64 (theta_N, phi_N),
+    vis_q [V][4**log2k] (qtree layout), light [batch][stride >= 4**log2k] (HAAR1 prefixes)
+    -> radiance [V][batch] = integral of L_b * Rot(theta_v, phi_v) rho * V_v (the paper's shading:
+    the BRDF rotated per normal, then the triple product)."""
+    lib = load()
+    _dev_f32(brdf, "brdf")
+    _dev_f32(vis_q, "vis_q")
+    _dev_f32(light, "light")
+    log2n = _log2n_pow4(brdf.numel(), "brdf")
+    nrm = np.ascontiguousarray(np.asarray(normals, dtype=np.float64))
+    V = vis_q.shape[0]
+    kf = 4 ** log2k
+    if nrm.shape != (V, 2):
+        raise ValueError("normals must be [V][2] (theta_N, phi_N)")
+    if vis_q.dim() != 2 or vis_q.shape[1] != kf:
+        raise ValueError("vis_q must be [V][4**log2k]")
+    if light.dim() != 2 or light.shape[1] < kf:
+        raise ValueError("light must be [batch][stride >= 4**log2k]")
+    B, stride = light.shape
+    out = _out(out, (V, B), vis_q.device)
+    need = relight_brdf_rotated_workspace_bytes(log2n, log2k, B)
+    workspace = _aligned_workspace(need, workspace, vis_q.device)
+    st = lib.relight_vertices_brdf_rotated(brdf.data_ptr(), log2n, nrm.ctypes.data, V, vis_q.data_ptr(), log2k,
+                                           light.data_ptr(), stride, B, out.data_ptr(), workspace.data_ptr(), need,
+                                           _stream_ptr(stream))
+    check("relight_vertices_brdf_rotated", st)
+    return out
+
+
 def hs_fill_sparse_transfer(indices: torch.Tensor, values: torch.Tensor, row_start: int, faces: int, log2n: int,
                             dense_levels: int, seed: int, stream: Optional[torch.cuda.Stream] = None):
     """Fill indices/values [rows][K_s] with synth.sparse_transfer_rows (bit for bit)."""

@@ -372,6 +372,44 @@ hs_status haar_rotate_coeffs(const float* in, float* out, int log2n, int batch, 
   return s;
 }
 
+size_t relight_brdf_rotated_workspace_bytes(int log2n, int log2k, int batch) {
+  if (log2n < 3 || log2n > 11 || log2k < 3 || log2k > log2n || batch < 1 || batch > 1024) return 0;
+  return brdf_rotated_workspace_bytes_impl(log2n, log2k, batch);
+}
+
+hs_status relight_vertices_brdf_rotated(const float* brdf, int log2n, const double* normals_host, int64_t num_vertices,
+                                        const float* vis_q, int log2k, const float* light, int64_t light_stride,
+                                        int batch, float* radiance, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+  g_last_launches = 0;
+  g_launches = 0;
+  if (!brdf || !normals_host || !vis_q || !light || !radiance || !workspace) return HS_ERR_INVALID_ARG;
+  if (log2n < 3 || log2n > 11 || log2k < 3 || log2k > log2n || num_vertices < 1 || batch < 1 || batch > 1024)
+    return HS_ERR_INVALID_ARG;
+  const long long kf = 1ll << (2 * log2k);
+  if (light_stride < kf || (light_stride & 3)) return HS_ERR_INVALID_ARG;
+  for (long long i = 0; i < 2ll * num_vertices; ++i)
+    if (!std::isfinite(normals_host[i])) return HS_ERR_INVALID_ARG;
+  if (workspace_bytes < brdf_rotated_workspace_bytes_impl(log2n, log2k, batch)) return HS_ERR_INVALID_ARG;
+  {
+    const size_t rb = (size_t)num_vertices * batch * sizeof(float);
+    if (overlap(radiance, rb, brdf, ((size_t)1 << (2 * log2n)) * 4) ||
+        overlap(radiance, rb, vis_q, (size_t)num_vertices * kf * 4) ||
+        overlap(radiance, rb, light, span_bytes(batch, light_stride, kf)) || overlap(radiance, rb, workspace, workspace_bytes))
+      return HS_ERR_INVALID_ARG;
+  }
+  if (!aligned16(brdf) || !aligned16(vis_q) || !aligned16(light) ||
+      !aligned_to(radiance, relight_tc_eligible(1, (int)kf, batch) ? 16 : 4) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 1023))
+    return HS_ERR_ALIGNMENT;
+  hs_status s = check_device();
+  if (s != HS_OK) return s;
+  s = launch_relight_brdf_rotated(brdf, log2n, normals_host, num_vertices, vis_q, log2k, light, light_stride, batch,
+                                  radiance, workspace, workspace_bytes, (cudaStream_t)stream);
+  g_last_launches = g_launches;
+  return s;
+}
+
 hs_status haar_pack_qtree(const float* in, int64_t rows, int faces, int64_t in_face_stride, int log2k, float* out,
                           void* stream) {
   g_last_launches = 0;

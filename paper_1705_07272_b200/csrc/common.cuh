@@ -191,7 +191,11 @@ hs_status launch_relight_triple(const float* brdf_q, const float* vis_q, long lo
                                 cudaStream_t st);
 size_t rotate_workspace_bytes_impl(int log2n, long long maps);
 hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
-                        size_t ws_bytes, cudaStream_t st);
+                        size_t ws_bytes, cudaStream_t st, bool bcast = false);   // bcast: one source pyramid for all maps
+size_t brdf_rotated_workspace_bytes_impl(int log2n, int log2k, int batch);
+hs_status launch_relight_brdf_rotated(const float* brdf, int log2n, const double* normals, long long V, const float* vis_q,
+                                      int log2k, const float* light, long long lstride, int batch, float* R, void* ws,
+                                      size_t ws_bytes, cudaStream_t st);
 hs_status launch_fill_transfer(float* out, long long row_start, long long rows, int faces,
                                int kface, uint64_t seed, uint64_t stream_id, cudaStream_t st);
 

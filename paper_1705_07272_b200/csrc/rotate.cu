@@ -196,7 +196,7 @@ __global__ void rot_pole_kernel(const double* __restrict__ F, int n, double* __r
 constexpr int kTS = 16;
 __global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const double* __restrict__ F, const double* __restrict__ E,
                                                                   int n, const __grid_constant__ RotParams prm, Trig tr,
-                                                                  double* __restrict__ Gf) {
+                                                                  double* __restrict__ Gf, int fmaps) {
   __shared__ Ang C[kTS + 1][kTS + 1];
   const int N = 1 << n;
   const int TS = N < kTS ? N : kTS;
@@ -215,9 +215,10 @@ __global__ void __launch_bounds__(kTS * kTS) rot_chainrule_kernel(const double* 
   const int ti = threadIdx.x / TS, tj = threadIdx.x - ti * TS;
   const int i = i0 + ti, j = j0 + tj;
   const double iT = (double)N / 3.141592653589793, iP = (double)N / 6.283185307179586;
-  const double* Xf = F + (long long)b * 2 * NN;
+  const long long fb = fmaps ? b : 0;   // fmaps = 0: one source map shared by every rotation
+  const double* Xf = F + fb * 2 * NN;
   const double* Yf = Xf + NN;
-  const double* Eb = E + (long long)b * 4 * N;
+  const double* Eb = E + fb * 4 * N;
   const Ang A0 = C[ti][tj];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
@@ -292,14 +293,14 @@ __global__ void rot_bottomup_kernel(const double* __restrict__ src, int src_plan
 }
 
 // ------------------------------------------------------------------------------- scaling
-__global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ in, int n, long long map0,
-                                                     const __grid_constant__ RotParams prm, Trig tr,
+__global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ in, long long in_stride, int n,
+                                                     long long map0, const __grid_constant__ RotParams prm, Trig tr,
                                                      float* __restrict__ out) {
   __shared__ float A[2][1 << (2 * kDcLevel)];
   __shared__ float red[8];
   const long long b = blockIdx.x;
   const long long NN = 1ll << (2 * n);
-  const float* src = in + b * NN;
+  const float* src = in + b * in_stride;
   const int L = n < kDcLevel ? n : kDcLevel;
   if (threadIdx.x == 0) A[0][0] = __ldg(src);
   __syncthreads();
@@ -377,7 +378,7 @@ size_t rotate_workspace_bytes_impl(int log2n, long long maps) {
 }
 
 hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
-                        size_t ws_bytes, cudaStream_t st) {
+                        size_t ws_bytes, cudaStream_t st, bool bcast) {
   const long long NN = 1ll << (2 * n);
   const size_t mcap = (size_t)(maps < kRotChunk ? maps : kRotChunk);
   const size_t fd = (mcap * 2 * (size_t)NN * sizeof(double) + 255) & ~size_t(255);
@@ -405,24 +406,27 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
       prm.ca[k] = std::cos(angles[2 * (m0 + k)]);
       prm.sa[k] = std::sin(angles[2 * (m0 + k)]);
     }
-    const float* src = in + m0 * NN;
+    // bcast: every map rotates the same source pyramid -- its fields and pole rows are built once
+    const float* src = bcast ? in : in + m0 * NN;
+    const long long mf = bcast ? 1 : mc;
     float* dtmp = tmp + m0 * NN;
     // (1) top-down to the finest fields (ping-pong between bufA and bufB)
     double* cur = bufB;
     for (int l = 0; l < n; ++l) {
       double* nxt = (cur == bufA) ? bufB : bufA;
-      rot_topdown_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(src, mc, n, l, cur, nxt);
+      rot_topdown_kernel<<<grid_for(mf << (2 * l)), 256, 0, st>>>(src, mf, n, l, cur, nxt);
       HS_CHECK_LAUNCH("rot_topdown_kernel");
       cur = nxt;
     }
     // (2) pole rows, chain rule, closure
-    rot_pole_kernel<<<(unsigned)mc, 256, 0, st>>>(cur, n, poles);
+    rot_pole_kernel<<<(unsigned)mf, 256, 0, st>>>(cur, n, poles);
     HS_CHECK_LAUNCH("rot_pole_kernel");
     {
       const int TS = (1 << n) < kTS ? (1 << n) : kTS;
       const int tiles = (int)(NN / ((long long)TS * TS));
       const int thr = (TS + 1) * (TS + 1) > TS * TS ? ((TS * TS + 31) / 32) * 32 : TS * TS;
-      rot_chainrule_kernel<<<dim3(tiles, (unsigned)mc), thr < 32 ? 32 : thr, 0, st>>>(cur, poles, n, prm, tr, Gf);
+      rot_chainrule_kernel<<<dim3(tiles, (unsigned)mc), thr < 32 ? 32 : thr, 0, st>>>(cur, poles, n, prm, tr, Gf,
+                                                                                       bcast ? 0 : 1);
     }
     HS_CHECK_LAUNCH("rot_chainrule_kernel");
     rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
@@ -438,7 +442,7 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
       planes = 3;
       d = (d == bufA) ? bufB : bufA;
     }
-    rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, n, 0, prm, tr, dtmp);
+    rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, bcast ? 0 : NN, n, 0, prm, tr, dtmp);
     HS_CHECK_LAUNCH("rot_dc_kernel");
   }
   // azimuth: the exact shift by beta N / (2 pi) columns

@@ -14,7 +14,7 @@ import sys
 KEEP = re.compile(r"^(Kernel Name|dram__bytes|gpu__dram_throughput|gpu__time_duration|l1tex__data_bank_conflicts_pipe_lsu_mem_shared|"
                   r"l1tex__data_pipe_lsu_wavefronts_mem_shared|launch__|sm__cycles_elapsed\.avg|sm__pipe_tensor_cycles_active|"
                   r"smsp__issue_active|sm__warps_active|smsp__inst_executed\.sum|sm__throughput|lts__t_bytes\.sum|"
-                  r"gpu__compute_memory_throughput)")
+                  r"gpu__compute_memory_throughput|sm__pipe_fp64_cycles_active|sm__inst_executed_pipe_xu|l1tex__data_pipe_lsu_wavefronts\.sum)")
 
 
 def main(rep, out):

@@ -393,6 +393,10 @@ CONFIGS = {
                   "row f1: 4096 lat-long maps of 64 x 64 (BRDF-like, smooth), each rotated by its own (alpha, beta)"),
     "c5t": Config("c5t", 8, 6, 1000000, 5, 64, SEED_BASE + 5,
                   "c5 with the triple product (row f3): per-vertex BRDF and visibility, each 6 x 1024 coefficients"),
+    "c7s": Config("c7s", 6, 1, 16384, 5, 64, SEED_BASE + 7,
+                  "rows f1 + f3, the paper's shading: 64 frames of a 64 x 64 lat-long HDR light shifted to the "
+                  "1024-coefficient band, one smooth BRDF rotated per vertex normal in the Haar domain, "
+                  "per-vertex visibility, triple product; 16384 vertices"),
 }
 
 

@@ -145,6 +145,19 @@ def test_widened_entries_validate_before_device(lib):
     c = lib.haar_shift_coeffs_coarse
     assert c(FAKE, FAKE * 4, 8, 9, 6, 1, ap, 5, W, 1 << 30, None) == 1                          # L > n
     assert c(FAKE, FAKE * 4, 8, 5, 6, 1, ap, 6, W, 1 << 30, None) == 1                          # band > L
+    br = lib.relight_vertices_brdf_rotated
+    nrm = np.zeros(2 * 100)
+    npp = nrm.ctypes.data_as(ctypes.c_void_p)
+    bneed = lib.relight_brdf_rotated_workspace_bytes(6, 5, 64)
+    assert bneed > 0 and lib.relight_brdf_rotated_workspace_bytes(6, 7, 64) == 0                # k > n
+    assert br(None, 6, npp, 100, FAKE * 2, 5, FAKE * 3, 4096, 64, FAKE * 4, W, bneed, None) == 1  # null brdf
+    assert br(FAKE, 6, npp, 100, FAKE * 2, 2, FAKE * 3, 4096, 64, FAKE * 4, W, bneed, None) == 1  # log2k < 3
+    assert br(FAKE, 6, npp, 100, FAKE * 2, 5, FAKE * 3, 512, 64, FAKE * 4, W, bneed, None) == 1   # stride < 4^k
+    assert br(FAKE, 6, npp, 100, FAKE * 2, 5, FAKE * 3, 4096, 64, FAKE * 4, W, bneed - 1, None) == 1  # small ws
+    nrm[7] = np.inf
+    assert br(FAKE, 6, npp, 100, FAKE * 2, 5, FAKE * 3, 4096, 64, FAKE * 4, W, bneed, None) == 1  # non-finite normal
+    nrm[7] = 0.0
+    assert br(FAKE, 6, npp, 100, FAKE * 2, 5, FAKE * 3, 4096, 64, FAKE * 4, W + 512, bneed, None) == 2  # ws align
     assert lib.hs_enable_peer_access(-1) in (1, 4)
 
 
