@@ -68,7 +68,11 @@ typedef enum {
  *           the phi-axis"), P:331/P:408/P:463 (coefficients are finite differences), eq:pde1-2
  *           P:416-425 with identity Jacobian (the difference fields translate), eq:conv/eq:tker/
  *           eq:sker P:466-478 and P:486-497 (recursive [1,1] x [1,2,1] synthesis, O(N))
- *           (start at a coarser level: exact here for dyadic shifts).  No inverse transform.
+ *           (start at a coarser level: exact here for dyadic shifts).  Working levels m = 6..9
+ *           (fractional shifts at N = 64..512) carry the fields' common antiderivative -- the
+ *           level-m approximation of the shifted window rows, from the details only (scaling
+ *           coefficient 0) -- in one fp64 field instead of three difference fields; the recursions
+ *           are the same linear maps (DESIGN.md §4.1 "Band kernel").
  *
  *   in, out       [batch][faces][K] fp32, K = N*N (ndim = 2) or N (ndim = 1), HAAR1 order.
  *                 out must not overlap in.  With band_levels < log2n, out is
@@ -83,8 +87,8 @@ typedef enum {
  *   workspace     device scratch of at least haar_shift_workspace_bytes(...) bytes (may be NULL
  *                 when that size is 0).  Contents on entry are irrelevant.
  * Result: out = S_s in, equal to forward(box_shift(inverse(in))) within fp32 output rounding:
- * the 2D difference fields are carried in fp64 at every size because fp32 field rounding is
- * amplified ~2^(n-l) on the coarse outputs.
+ * the 2D fields are carried in fp64 at every size because fp32 field rounding is amplified
+ * ~2^(n-l) on the coarse outputs.
  * ------------------------------------------------------------------------------------------- */
 HS_API hs_status haar_shift_coeffs(const float* in, float* out, int ndim, int log2n, int faces,
                             int batch, const double* shifts_host, int band_levels,

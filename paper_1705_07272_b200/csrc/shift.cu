@@ -10,7 +10,7 @@
 
 namespace hs {
 
-hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, bool any_tile, bool any_stream,
+hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_perm, bool any_tile, int max_band_m,
                          cudaStream_t st);
 int shift2d_tiles_for(int m);
 
@@ -144,19 +144,21 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     a.out_face_stride = (int)Kb;
     a.num_faces = nf;
     int max_tiles = 0;
-    bool any_perm = false, any_coarse = false, any_tile = false, any_stream = false;
-    // the streaming kernel reads float4 detail rows and writes float4 output rows
-    a.stream = (ndim == 2 && aligned16(a.in) && aligned16(a.out) && in_batch_stride % 4 == 0 &&
-                in_face_stride % 4 == 0 && (Kb % 4 == 0)) ? 1 : 0;
+    bool any_perm = false, any_coarse = false, any_tile = false;
+    int max_band_m = 0;   // largest working level taken by the band kernel (0: none)
+    a.stream = (ndim == 2) ? 1 : 0;
     if (shifts_host) {
       for (int i = 0; i < nf; ++i) {
         const double* s = shifts_host + (g0 + i) * ndim;
         a.fp[i] = (ndim == 2) ? make_face_param_2d(s[0], s[1], n) : make_face_param_1d(s[0], n);
         max_tiles = std::max(max_tiles, shift2d_tiles_for(a.fp[i].m));
         if (a.fp[i].m < band || a.fp[i].m == 0) any_perm = true;
-        if (coarse_level(a.fp[i].m) > 0) any_coarse = true;
-        if (a.stream && stream_level(a.fp[i].m)) any_stream = true;
-        else if (a.fp[i].m > 0) any_tile = true;
+        if (a.stream && stream_level(a.fp[i].m)) {
+          max_band_m = std::max(max_band_m, a.fp[i].m);
+        } else if (a.fp[i].m > 0) {
+          any_tile = true;
+          if (coarse_level(a.fp[i].m) > 0) any_coarse = true;
+        }
       }
     } else {
       // per-vertex device shifts: FaceParams computed on the device (one per vertex and face)
@@ -170,10 +172,10 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
       any_perm = true;
       any_coarse = coarse_level(n) > 0;
       any_tile = true;
-      any_stream = a.stream && n >= kStreamMinLevel;
+      max_band_m = (a.stream && n >= kStreamMinLevel) ? std::min(n, kStreamMaxLevel) : 0;
     }
     if (ndim == 2) {
-      hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, any_tile, any_stream, st);
+      hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, any_tile, max_band_m, st);
       if (s != HS_OK) return s;
     } else {
       const size_t smem = (size_t)2 * (1u << n) * sizeof(double);

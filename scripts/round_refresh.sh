@@ -18,14 +18,14 @@ timeout 300 $CMD > /dev/null 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
     --log-file $OUT/launches_c5.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "launch-list exit=$?" >> $OUT/status.txt
-timeout 1200 $NCU -k regex:"relight_tc_kernel|shift2d_stream_kernel|coarse_fields_kernel|coarse_finish_kernel" \
+timeout 1200 $NCU -k regex:"relight_tc_kernel|shift2d_band_kernel|band_finish_kernel" \
     -c 4 -o $OUT/prof_c5 $CMD > $OUT/ncu_c5.log 2>&1
 echo "ncu c5 exit=$?" >> $OUT/status.txt
 timeout 300 python scripts/run_c4.py 20000 1 > /dev/null 2>&1 && \
 timeout 900 $NCU -k regex:"planes_(a|c|low)_kernel" -c 3 -o $OUT/prof_c4 python scripts/run_c4.py 20000 1 \
     > $OUT/ncu_c4.log 2>&1
 echo "ncu c4 exit=$?" >> $OUT/status.txt
-declare -A KRX=([c3]="shift2d_stream|coarse_f|relight_gemv" [c2]="shift2d_small|relight_gemv_short" [c6r]="rot_")
+declare -A KRX=([c3]="shift2d_band|band_finish|relight_gemv" [c2]="shift2d_small|relight_gemv_short" [c6r]="rot_")
 for c in c3 c2 c6r; do
   C2="python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
   timeout 300 $C2 > /dev/null 2>&1 && \
