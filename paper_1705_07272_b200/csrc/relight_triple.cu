@@ -127,47 +127,45 @@ __device__ __forceinline__ void triple_chunk(LDR ld_r, LDV ld_v, float w0, float
 
 // ------------------------------------------------------------------------------- packing
 // out[row][f][c*64 + s] from in[row*faces*in_face_stride + f*in_face_stride + HAAR1 index]
-__global__ void pack_qtree_kernel(const float* __restrict__ in, long long rows, int faces, long long in_face_stride,
-                                  int k, float* __restrict__ out) {
+// One thread per output slot: grid.x over the 4^k slots of one face band, grid.y = row * faces + f.
+// (A flat grid-stride form with 64-bit index math ran at 0.3 TB/s: 102 us for 4096 BRDF rows.)
+__global__ void __launch_bounds__(256) pack_qtree_kernel(const float* __restrict__ in, int faces,
+                                                         long long in_face_stride, int k, float* __restrict__ out) {
   const int r = k - 3;
-  const long long kf = 1ll << (2 * k);
-  const long long total = rows * faces * kf;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long rf = e >> (2 * k);         // row * faces + f
-    const int pos = (int)(e & (kf - 1));
-    const float* src = in + rf * in_face_stride;
-    const int c = pos >> 6, s = pos & 63;
-    const int ci = c >> r, cj = c & ((1 << r) - 1);
-    float v;
-    if (s == 63) {
-      float a = __ldg(src);
-      for (int l = 0; l < r; ++l) {
-        const int ai = ci >> (r - l), aj = cj >> (r - l);
-        const int q = (((ci >> (r - l - 1)) & 1) << 1) | ((cj >> (r - l - 1)) & 1);
-        const int base = (1 << (2 * l)), cell = ai * (1 << l) + aj;
-        const float h = __ldg(src + base + cell), vv = __ldg(src + 2 * base + cell), d = __ldg(src + 3 * base + cell);
-        a = fmaf(ldexpf(1.f, l), sgn_h(q) * h + sgn_v(q) * vv + sgn_d(q) * d, a);
-      }
-      v = a;
-    } else {
-      int l, t, i, j;
-      if (s >= 60) {
-        l = r, t = s - 60, i = ci, j = cj;
-      } else {
-        const int q = s / 15, u = s % 15;
-        const int i1 = 2 * ci + (q >> 1), j1 = 2 * cj + (q & 1);
-        if (u >= 12) {
-          l = r + 1, t = u - 12, i = i1, j = j1;
-        } else {
-          const int p = u / 3;
-          l = r + 2, t = u % 3, i = 2 * i1 + (p >> 1), j = 2 * j1 + (p & 1);
-        }
-      }
-      v = __ldg(src + (1ll << (2 * l)) * (1 + t) + (long long)i * (1 << l) + j);
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= (1 << (2 * k))) return;
+  const long long rf = blockIdx.y + (long long)blockIdx.z * gridDim.y;   // row * faces + f
+  const float* src = in + rf * in_face_stride;
+  const int c = pos >> 6, s = pos & 63;
+  const int ci = c >> r, cj = c & ((1 << r) - 1);
+  float v;
+  if (s == 63) {
+    float a = __ldg(src);
+    for (int l = 0; l < r; ++l) {
+      const int ai = ci >> (r - l), aj = cj >> (r - l);
+      const int q = (((ci >> (r - l - 1)) & 1) << 1) | ((cj >> (r - l - 1)) & 1);
+      const int base = (1 << (2 * l)), cell = ai * (1 << l) + aj;
+      const float h = __ldg(src + base + cell), vv = __ldg(src + 2 * base + cell), d = __ldg(src + 3 * base + cell);
+      a = fmaf(ldexpf(1.f, l), sgn_h(q) * h + sgn_v(q) * vv + sgn_d(q) * d, a);
     }
-    out[e] = v;
+    v = a;
+  } else {
+    int l, t, i, j;
+    if (s >= 60) {
+      l = r, t = s - 60, i = ci, j = cj;
+    } else {
+      const int q = s / 15, u = s - 15 * q;
+      const int i1 = 2 * ci + (q >> 1), j1 = 2 * cj + (q & 1);
+      if (u >= 12) {
+        l = r + 1, t = u - 12, i = i1, j = j1;
+      } else {
+        const int p = u / 3;
+        l = r + 2, t = u - 3 * p, i = 2 * i1 + (p >> 1), j = 2 * j1 + (p & 1);
+      }
+    }
+    v = __ldg(src + (1 << (2 * l)) * (1 + t) + i * (1 << l) + j);
   }
+  out[(rf << (2 * k)) + pos] = v;
 }
 
 // ------------------------------------------------------------------------------- CUDA-core fallback
@@ -492,11 +490,20 @@ struct TripleRow {   // the tripling terms of a row, chunk by chunk (relight_red
 
 hs_status launch_pack_qtree(const float* in, long long rows, int faces, long long in_face_stride, int log2k,
                             float* out, cudaStream_t st) {
-  const long long total = rows * faces * (1ll << (2 * log2k));
-  long long blocks = (total + 255) / 256;
-  if (blocks > (long long)num_sms() * 16) blocks = (long long)num_sms() * 16;
-  if (blocks < 1) blocks = 1;
-  pack_qtree_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, rows, faces, in_face_stride, log2k, out);
+  const long long rf = rows * faces;
+  if (rf <= 0) return HS_OK;
+  const unsigned gy = (unsigned)(rf < 65535 ? rf : 65535);
+  const unsigned gz = (unsigned)((rf + gy - 1) / gy);
+  if ((long long)gy * gz != rf) {   // ragged: launch the full 65535-row slabs, then the rest
+    const long long full = (rf / gy) * gy;
+    pack_qtree_kernel<<<dim3((unsigned)((1 << (2 * log2k)) + 255) / 256, gy, (unsigned)(rf / gy)), 256, 0, st>>>(
+        in, faces, in_face_stride, log2k, out);
+    HS_CHECK_LAUNCH("pack_qtree_kernel");
+    return launch_pack_qtree(in + full * in_face_stride, rf - full, 1, in_face_stride, log2k,
+                             out + (full << (2 * log2k)), st);
+  }
+  pack_qtree_kernel<<<dim3((unsigned)((1 << (2 * log2k)) + 255) / 256, gy, gz), 256, 0, st>>>(in, faces, in_face_stride,
+                                                                                           log2k, out);
   HS_CHECK_LAUNCH("pack_qtree_kernel");
   return HS_OK;
 }
