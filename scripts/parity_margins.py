@@ -90,6 +90,27 @@ got6 = hs.haar_rotate_coeffs(t(maps6), ang6).cpu().numpy()
 pick = rng.integers(0, cfg6.frames, 16)
 out["c6r rotated maps (16 sampled, max)"] = max(rel(got6[b], orot.rotate_coeffs_chain(maps6[b], *ang6[b]))
                                                 for b in pick)
+# c7s: the composed shading (rows f1 + f3) on the bench's inputs, 16384 vertices, 24 sampled
+# vertices against the chain-rule oracle + the pixel-domain triple integral
+cfg7 = synth.config("c7s")
+n7, B7, k7, kf7, V7 = cfg7.log2n, cfg7.frames, cfg7.band_levels, cfg7.k_face, cfg7.vertices
+brdf7 = synth.smooth_sphere_maps(cfg7.seed, 1, n7)[0]
+vis7 = synth.shading_rows(cfg7.seed, 0, V7, 1, kf7, synth.STREAM_VIS)
+vq7 = hs.haar_pack_qtree(t(vis7).view(V7, 1, kf7), k7).view(V7, kf7)
+rng7 = np.random.default_rng([cfg7.seed, 7])
+nv7 = rng7.normal(size=(V7, 3))
+nv7 /= np.linalg.norm(nv7, axis=1, keepdims=True)
+nrm7 = np.stack([np.arccos(np.clip(nv7[:, 1], -1.0, 1.0)), np.mod(np.arctan2(nv7[:, 0], nv7[:, 2]), 2 * np.pi)], 1)
+L7 = synth.light_pyramids(cfg7.seed, B7, 1, n7)
+sh7 = np.stack([np.zeros(B7), np.arange(B7) * (1 << n7) / 64.0], axis=1)[:, None, :]
+band7 = hs.haar_shift_coeffs(t(L7), sh7, 2, k7)
+R7 = hs.relight_vertices_brdf_rotated(t(brdf7), nrm7, vq7, band7.view(B7, kf7), k7).cpu().numpy()
+rows7 = rng.integers(0, V7, 24)
+rho7 = np.stack([orot.rotate_coeffs_chain(brdf7.astype(np.float64), float(nrm7[v, 0]), float(nrm7[v, 1]))[:kf7]
+                 for v in rows7])
+Lb7 = oshift.shift_coeffs(L7, sh7, 2)[:, :, :kf7]
+out["c7s radiance (24 sampled vertices)"] = rel(R7[rows7], orelight.relight_triple(rho7, vis7[rows7].astype(np.float64),
+                                                                                  Lb7, 1, kf7))
 torch.cuda.synchronize()
 for k, v in out.items():
     print(f"{k:42s} {v:.3e}  ({'ok' if v <= 1e-5 else 'OVER'}; margin x{1e-5 / v:.1f})")
