@@ -18,13 +18,17 @@ namespace {
 
 constexpr int k1DThreads = 256;
 
-// 1D exact difference-domain shift, one CTA per signal:
+// 1D shift, one CTA per signal.  The paper's difference recursion
 //   Delta_l[k] = a_l[k] - a_l[k+1]; top-down Delta_{l+1}[2k] = 2 d^_l[k],
 //   Delta_{l+1}[2k+1] = Delta_l[k] - d^_l[k] - d^_l[k+1]; shift at level m;
-//   bottom-up d^'_l[k] = Delta'_{l+1}[2k] / 2, Delta'_l[k] = (D'[2k] + 2 D'[2k+1] + D'[2k+2]) / 2.
-// The differences are carried in fp64 (one rounding per output): fp32 rounding of the fine
-// differences is amplified ~2^(n-l) on a coarse band (1.2e-5 measured for white
-// noise at N = 2048-4096 in fp32).
+//   bottom-up d^'_l[k] = Delta'_{l+1}[2k] / 2, Delta'_l[k] = (D'[2k] + 2 D'[2k+1] + D'[2k+2]) / 2
+// is carried on its antiderivative a (as the 2D band kernel): a_0 = 0,
+// a_{l+1}[2k] = a_l[k] + d^_l[k], a_{l+1}[2k+1] = a_l[k] - d^_l[k]; a' = w0 a[x - Q] + w1 a[x - Q - 1];
+// d^'_l[k] = (a'[2k] - a'[2k+1]) / 2 (= Delta'[2k] / 2), a'_l[k] = (a'[2k] + a'[2k+1]) / 2 (whose
+// difference is the [1,2,1] / 2 recursion above).  The signal's levels < m are staged into shared
+// memory in one round trip (one global load per level made the kernel latency-bound: 60 us for
+// 4096 signals of 4096); fp64 in shared memory (one rounding per output: fp32 rounding of the fine
+// values is amplified ~2^(n-l) on a coarse band).
 __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_constant__ ShiftArgs args) {
   extern __shared__ __align__(16) double smem[];
   const int g = blockIdx.x;
@@ -36,8 +40,10 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   const int band = args.band;
   const int Kb = 1 << band;
-  double* d0 = smem;      // N doubles: Delta at the current level
-  double* d1 = smem + N;  // N doubles
+  const int gm = 1 << m;
+  double* cur = smem;                                        // 2^m doubles
+  double* nxt = smem + gm;                                   // 2^m doubles
+  float* S = reinterpret_cast<float*>(smem + 2 * gm);        // in[0 .. 2^m): levels < m
   // levels >= m: permutation by q / 2^(n-l); scaling copied
   for (int idx = threadIdx.x; idx < Kb; idx += blockDim.x) {
     if (idx == 0) {
@@ -51,27 +57,28 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
     out[idx] = in[(1 << l) + sk];
   }
   if (m == 0) return;
-  // top-down Delta_1 .. Delta_m  (Delta_0 = 0)
-  double* cur = d0;
-  double* nxt = d1;
-  if (threadIdx.x == 0) cur[0] = 0.0;
+  (void)N;
+  if ((reinterpret_cast<unsigned long long>(in) & 15) == 0 && gm >= 4) {
+    for (int idx = threadIdx.x; idx < gm / 4; idx += blockDim.x)
+      reinterpret_cast<float4*>(S)[idx] = __ldg(reinterpret_cast<const float4*>(in) + idx);
+  } else {
+    for (int idx = threadIdx.x; idx < gm; idx += blockDim.x) S[idx] = __ldg(in + idx);
+  }
+  if (threadIdx.x == 0) cur[0] = 0.0;   // a_0 = 0: the scaling coefficient drops out of every output
   __syncthreads();
   for (int l = 0; l < m; ++l) {
     const int gl = 1 << l;
     const double asc = exp2((double)l * 0.5);  // unit-interval -> averaging: x 2^(l/2)
     for (int kk = threadIdx.x; kk < gl; kk += blockDim.x) {
-      const double dk = (double)in[gl + kk] * asc;
-      const double dk1 = (double)in[gl + ((kk + 1) & (gl - 1))] * asc;
-      nxt[2 * kk] = 2.0 * dk;
-      nxt[2 * kk + 1] = cur[kk] - dk - dk1;
+      const double a = cur[kk], d = (double)S[gl + kk] * asc;
+      *reinterpret_cast<double2*>(nxt + 2 * kk) = make_double2(a + d, a - d);
     }
     __syncthreads();
     double* t = cur;
     cur = nxt;
     nxt = t;
   }
-  // shift at level m, then bottom-up m-1 .. 0
-  const int gm = 1 << m;
+  // shift at level m, then the analysis m-1 .. 0
   const double w0 = 1.0 - (double)P.wx, w1 = (double)P.wx;
   for (int x = threadIdx.x; x < gm; x += blockDim.x)
     nxt[x] = w0 * cur[(x - P.Qx) & (gm - 1)] + w1 * cur[(x - P.Qx - 1) & (gm - 1)];
@@ -82,12 +89,12 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
     nxt = t;
   }
   for (int l = m - 1; l >= 0; --l) {
-    const int gl = 1 << l, G = 2 * gl;
+    const int gl = 1 << l;
     const double osc = exp2(-(double)l * 0.5);
     for (int kk = threadIdx.x; kk < gl; kk += blockDim.x) {
-      const double a0 = cur[2 * kk], a1 = cur[2 * kk + 1], a2 = cur[(2 * kk + 2) & (G - 1)];
-      nxt[kk] = 0.5 * (a0 + 2.0 * a1 + a2);
-      if (l < band) out[gl + kk] = (float)(0.5 * a0 * osc);
+      const double2 a = *reinterpret_cast<const double2*>(cur + 2 * kk);
+      nxt[kk] = 0.5 * (a.x + a.y);
+      if (l < band) out[gl + kk] = (float)(0.5 * (a.x - a.y) * osc);
     }
     __syncthreads();
     double* t = cur;
@@ -178,7 +185,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
       hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, any_tile, max_band_m, st);
       if (s != HS_OK) return s;
     } else {
-      const size_t smem = (size_t)2 * (1u << n) * sizeof(double);
+      const size_t smem = (size_t)2 * (1u << n) * sizeof(double) + (size_t)(1u << n) * sizeof(float);
       if (smem > 48 * 1024) {
         HS_SMEM_ATTR(shift1d_kernel, smem);
       }
