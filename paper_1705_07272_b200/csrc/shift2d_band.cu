@@ -95,14 +95,14 @@ template <int l, int NRL>
 __device__ __forceinline__ void topdown_step(const double* __restrict__ P, int pbase, int lo,
                                              const float* __restrict__ S, double* __restrict__ C) {
   constexpr int gl = 1 << l;
-  const double asc = p2d(l);
+  constexpr float asc = float(1u << l);   // unit -> averaging, exact in fp32 (|d| < 2^100)
   const double* Pr = P + (lo - pbase) * gl;
 #pragma unroll 2
   for (int idx = threadIdx.x; idx < NRL * gl; idx += kBandThreads) {
     const int rr = idx >> l, j = idx & (gl - 1);
     const double a = Pr[idx];
     const float* sd = S + idx;
-    const double H = (double)sd[0] * asc, V = (double)sd[NRL * gl] * asc, D = (double)sd[2 * NRL * gl] * asc;
+    const double H = (double)(sd[0] * asc), V = (double)(sd[NRL * gl] * asc), D = (double)(sd[2 * NRL * gl] * asc);
     const double p = a + V, q = a - V, s = H + D, t = H - D;
     double* c0 = C + (2 * rr) * (2 * gl) + 2 * j;
     *reinterpret_cast<double2*>(c0) = make_double2(p + s, p - s);
@@ -114,11 +114,24 @@ __device__ __forceinline__ void topdown_step(const double* __restrict__ P, int p
 // this lane's column sums e = s_top + s_bottom and differences d = s_top - s_bottom.  The block's
 // left lane gets the average and H, the right lane V and D.
 template <int X>
-__device__ __forceinline__ void lane_analyse(double e, double d, bool right, double& avg_or_v, double& h_or_d) {
+__device__ __forceinline__ void lane_analyse(double e, double d, bool right, double& sum, double& dif) {
+  // Unscaled (x 4 per level; the factors are folded into the emission scales): the block's left
+  // lane gets sum = e_l + e_r (4 avg) and dif = e_l - e_r (4 H); the right lane sum = d_l + d_r
+  // (4 V) and dif = d_r - d_l (-4 D: the sign is folded into the right lanes' scale).
+  const double own = right ? d : e;
   const double r = __shfl_xor_sync(0xffffffffu, right ? e : d, X);
-  // left: r = e of the right lane; right: r = d of the left lane
-  avg_or_v = right ? 0.25 * (r + d) : 0.25 * (e + r);
-  h_or_d = right ? 0.25 * (r - d) : 0.25 * (e - r);
+  sum = own + r;
+  dif = own - r;
+}
+
+// Emission of one analysis block's details: the left lane writes H (plane 1), the right lane V
+// (plane 2) and D (plane 3) -- one store per lane plus one predicated store, no divergent branch.
+__device__ __forceinline__ void emit(float* __restrict__ base, long long per, bool right, double sum, double dif,
+                                     double sc, double scd) {
+  const float v1 = (float)((right ? sum : dif) * sc);
+  float* p1 = right ? base + 2 * per : base + per;
+  *p1 = v1;
+  if (right) base[3 * per] = (float)(dif * scd);
 }
 
 // The last step M-1 -> M with the details already in registers (dr[k][t] for parent tid + k T).
@@ -126,7 +139,7 @@ template <int l, int NRL, int KP>
 __device__ __forceinline__ void topdown_last(const double* __restrict__ P, int pbase, int lo, const float (&dr)[KP][3],
                                              double* __restrict__ C) {
   constexpr int gl = 1 << l;
-  const double asc = p2d(l);
+  constexpr float asc = float(1u << l);
   const double* Pr = P + (lo - pbase) * gl;
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
@@ -134,7 +147,7 @@ __device__ __forceinline__ void topdown_last(const double* __restrict__ P, int p
     if (idx < NRL * gl) {
       const int rr = idx >> l, j = idx & (gl - 1);
       const double a = Pr[idx];
-      const double H = (double)dr[k][0] * asc, V = (double)dr[k][1] * asc, D = (double)dr[k][2] * asc;
+      const double H = (double)(dr[k][0] * asc), V = (double)(dr[k][1] * asc), D = (double)(dr[k][2] * asc);
       const double p = a + V, q = a - V, s = H + D, t = H - D;
       double* c0 = C + (2 * rr) * (2 * gl) + 2 * j;
       *reinterpret_cast<double2*>(c0) = make_double2(p + s, p - s);
@@ -257,10 +270,15 @@ __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam&
   constexpr int CPT = W >= kBandThreads ? W / kBandThreads : 1;
   if (tid < W) {
     const double* rows = bufA + (Slo - 2 * lo3) * W;   // source row Slo (0 or 1 rows into the buffer)
+    // emission scales: level M-k values are 4^k x (averaging units), output = unit = x 2^-(level)
+    const double sc1 = p2d(-(M + 1)), sc2 = p2d(-(M + 2)), sc3 = p2d(-(M + 3)), sc4 = p2d(-(M + 4));
 #pragma unroll 1
     for (int cc = 0; cc < CPT; ++cc) {
       const int c = tid + cc * kBandThreads;
+      const bool r1 = (c & 1) != 0, r2 = (c & 2) != 0, r4 = (c & 4) != 0, r8 = (c & 8) != 0;
       const int ca = (c - Qx) & (W - 1), cb = (c - Qx - 1) & (W - 1);
+      // output base of this lane's level M-1 block column (plane 0 offset; emit adds the planes)
+      float* const o1 = out + (R0 >> 1) * (W >> 1) + (c >> 1);
       double hprev = fma(wx0, rows[ca], wx1 * rows[cb]);
       double s_top = 0.0;                        // level M row 2i of the pair in flight
       double a1_top = 0.0, a2_top = 0.0, a3_top = 0.0;   // levels M-1, M-2, M-3 pending rows
@@ -277,18 +295,8 @@ __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam&
         // level M-1 block (row pair i = r / 2, column pair c >> 1)
         const int i1 = r >> 1;
         double x1, y1;
-        lane_analyse<1>(s_top + sv, s_top - sv, (c & 1) != 0, x1, y1);
-        if ((M - 1) < oband) {
-          const long long per = 1ll << (2 * (M - 1));
-          const double sc = p2d(-(M - 1));
-          const long long o = (long long)((R0 >> 1) + i1) * (W >> 1) + (c >> 1);
-          if (c & 1) {
-            out[2 * per + o] = (float)(x1 * sc);
-            out[3 * per + o] = (float)(y1 * sc);
-          } else {
-            out[per + o] = (float)(y1 * sc);
-          }
-        }
+        lane_analyse<1>(s_top + sv, s_top - sv, r1, x1, y1);
+        if ((M - 1) < oband) emit(o1 + i1 * (W >> 1), 1ll << (2 * (M - 1)), r1, x1, y1, sc1, -sc1);
         if ((i1 & 1) == 0) {
           a1_top = x1;
           continue;
@@ -296,18 +304,8 @@ __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam&
         // level M-2 (lanes c ^ 2; valid in lanes with c % 2 == 0)
         const int i2 = i1 >> 1;
         double x2, y2;
-        lane_analyse<2>(a1_top + x1, a1_top - x1, (c & 2) != 0, x2, y2);
-        if ((M - 2) < oband && (c & 1) == 0) {
-          const long long per = 1ll << (2 * (M - 2));
-          const double sc = p2d(-(M - 2));
-          const long long o = (long long)((R0 >> 2) + i2) * (W >> 2) + (c >> 2);
-          if (c & 2) {
-            out[2 * per + o] = (float)(x2 * sc);
-            out[3 * per + o] = (float)(y2 * sc);
-          } else {
-            out[per + o] = (float)(y2 * sc);
-          }
-        }
+        lane_analyse<2>(a1_top + x1, a1_top - x1, r2, x2, y2);
+        if ((M - 2) < oband && !r1) emit(out + ((R0 >> 2) + i2) * (W >> 2) + (c >> 2), 1ll << (2 * (M - 2)), r2, x2, y2, sc2, -sc2);
         if ((i2 & 1) == 0) {
           a2_top = x2;
           continue;
@@ -315,38 +313,19 @@ __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam&
         // level M-3 (lanes c ^ 4; valid in lanes with c % 4 == 0)
         const int i3 = i2 >> 1;
         double x3, y3;
-        lane_analyse<4>(a2_top + x2, a2_top - x2, (c & 4) != 0, x3, y3);
-        if ((M - 3) < oband && (c & 3) == 0) {
-          const long long per = 1ll << (2 * (M - 3));
-          const double sc = p2d(-(M - 3));
-          const long long o = (long long)((R0 >> 3) + i3) * (W >> 3) + (c >> 3);
-          if (c & 4) {
-            out[2 * per + o] = (float)(x3 * sc);
-            out[3 * per + o] = (float)(y3 * sc);
-          } else {
-            out[per + o] = (float)(y3 * sc);
-          }
-        }
+        lane_analyse<4>(a2_top + x2, a2_top - x2, r4, x3, y3);
+        if ((M - 3) < oband && (c & 3) == 0)
+          emit(out + ((R0 >> 3) + i3) * (W >> 3) + (c >> 3), 1ll << (2 * (M - 3)), r4, x3, y3, sc3, -sc3);
         if ((i3 & 1) == 0) {
           a3_top = x3;
           continue;
         }
         // level M-4 = L (lanes c ^ 8; valid in lanes with c % 8 == 0): one row per band
         double x4, y4;
-        lane_analyse<8>(a3_top + x3, a3_top - x3, (c & 8) != 0, x4, y4);
+        lane_analyse<8>(a3_top + x3, a3_top - x3, r8, x4, y4);
         if ((c & 7) == 0) {
-          const long long o = (long long)(R0 >> 4) * WL + (c >> 4);
-          if ((c & 8) == 0) wsA[o] = x4;   // A'_L
-          if (L < oband) {
-            const long long per = 1ll << (2 * L);
-            const double sc = p2d(-L);
-            if (c & 8) {
-              out[2 * per + o] = (float)(x4 * sc);
-              out[3 * per + o] = (float)(y4 * sc);
-            } else {
-              out[per + o] = (float)(y4 * sc);
-            }
-          }
+          if (!r8) wsA[(long long)(R0 >> 4) * WL + (c >> 4)] = x4 * p2d(-8);   // A'_L (x 4^-4)
+          if (L < oband) emit(out + (R0 >> 4) * WL + (c >> 4), 1ll << (2 * L), r8, x4, y4, sc4, -sc4);
         }
       }
     }
