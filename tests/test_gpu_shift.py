@@ -182,3 +182,24 @@ def test_deterministic_repeat():
 def test_launch_count_reported():
     _run(synth.random_signals(19, 1, 64)[None], np.array([[[0.5, 0.5]]]), 2)
     assert _hs().last_launch_count() >= 1
+
+
+@pytest.mark.parametrize("ndim,n", [(2, 6), (2, 8), (1, 5)])
+def test_unaligned_pointers_are_refused(ndim, n):
+    """The ABI contract (include/haarshift.h): in / out 16-byte aligned, HS_ERR_ALIGNMENT otherwise
+    -- checked before any launch.  (Faces inside a batch may sit at 8-byte offsets: 1D N = 2,
+    test_1d_sizes; the kernels take their scalar staging path there.)"""
+    import torch
+    hs = _hs()
+    from paper_1705_07272_b200._lib import HaarShiftError
+    N = 1 << n
+    K = N * N if ndim == 2 else N
+    B, F = 2, 2
+    sh = np.full((B, F, ndim), 0.25)
+    buf = torch.zeros(B * F * K + 1, device="cuda")
+    x = buf[1:].view(B, F, K)
+    with pytest.raises(HaarShiftError, match="ALIGNMENT"):
+        hs.haar_shift_coeffs(x, sh, ndim)
+    obuf = torch.zeros(B * F * K + 1, device="cuda")
+    with pytest.raises(HaarShiftError, match="ALIGNMENT"):
+        hs.haar_shift_coeffs(buf[:-1].view(B, F, K), sh, ndim, out=obuf[1:].view(B, F, K))
