@@ -19,15 +19,19 @@
 //                        f_Phi = -X_f / dphi interpolated bilinearly at the rotated midpoint
 //                        (Fig. 4; R26 -- increments instead of derivatives
 //                        keep the poles of the source finite);
-//   rot_closure_kernel   the periodic closure the Haar fields satisfy: every row of X sums to zero
+//   (closure)            the periodic closure the Haar fields satisfy: every row of X sums to zero
 //                        (Y needs none -- its last row reaches no output coefficient, only the
-//                        recursion's level-0 residual; tests/test_oracle_rotate.py);
+//                        recursion's level-0 residual; tests/test_oracle_rotate.py): the chain-rule
+//                        CTAs write partial row sums, the first bottom-up level subtracts the means;
 //   rot_bottomup_kernel  (3) the paper's recursion h_s = [1,1], h_t = [1,2,1], decimated by 2
 //                        (eq:conv-sker P:466-478) from (X_g, Y_g, Z_g = X_g[i] - X_g[i+1])
-//                        at the finest level down to level 0: every detail coefficient of g;
+//                        at the finest level down to level 5, one launch per level; then
+//   rot_tail_kernel      levels 4 .. 0 of each map in shared memory (one launch): every detail
+//                        coefficient of g;
 //   rot_dc_kernel        the scaling coefficient: mean of the level-L approximation of f
 //                        (L = min(n, 6), partial top-down in shared memory) resampled at the rotated
-//                        positions of the N x N grid (the paper is silent);
+//                        positions of the N x N grid (the paper is silent), each
+//                        rotated angle pair shared by a pixel and its mirror about phi = pi;
 // then haar_shift's kernels move the result by beta N / (2 pi) columns.
 #include <cuda_runtime.h>
 
@@ -236,10 +240,11 @@ __device__ __forceinline__ Ang mirror(Ang a) {
   a.Ph = (a.Ph == 0.0) ? 0.0 : 6.283185307179586 - a.Ph;
   return a;
 }
-__device__ __forceinline__ void chain_pixel(const double* __restrict__ Xf, const double* __restrict__ Yf,
-                                            const double* __restrict__ Eb, int N, Ang A0, Ang A1x, Ang A1y, Ang Mx,
-                                            Ang My, double* __restrict__ G, long long NN) {
+__device__ __forceinline__ double chain_pixel(const double* __restrict__ Xf, const double* __restrict__ Yf,
+                                              const double* __restrict__ Eb, int N, Ang A0, Ang A1x, Ang A1y, Ang Mx,
+                                              Ang My, double* __restrict__ G, long long NN) {
   const double iT = (double)N * 0.3183098861837907, iP = (double)N * 0.15915494309189535;
+  double xg = 0.0;
 #pragma unroll
   for (int t = 0; t < 2; ++t) {   // t = 0: X_g (neighbour in phi), t = 1: Y_g (neighbour in theta)
     const Ang A1 = t ? A1y : A1x;
@@ -251,13 +256,17 @@ __device__ __forceinline__ void chain_pixel(const double* __restrict__ Xf, const
     double dP = A0.Ph - A1.Ph;
     if (dP > 3.141592653589793) dP -= 6.283185307179586;
     if (dP < -3.141592653589793) dP += 6.283185307179586;
-    G[t * NN] = -yf * dT * iT - xf * dP * iP;
+    const double v = -yf * dT * iT - xf * dP * iP;
+    G[t * NN] = v;
+    if (t == 0) xg = v;
   }
+  return xg;
 }
 
 __global__ void __launch_bounds__(kTS * kTS, 4) rot_chainrule_kernel(const double* __restrict__ F, const double* __restrict__ E,
                                                                   int n, const __grid_constant__ RotParams prm, Trig tr,
-                                                                  double* __restrict__ Gf, int fmaps) {
+                                                                  double* __restrict__ Gf, int fmaps,
+                                                                  double* __restrict__ part) {
   __shared__ Ang C[kTS + 1][kTS + 2];    // centres: rows i0 .. i0 + TS, columns j0 - 1 .. j0 + TS
   __shared__ Ang MX[kTS][kTS + 1];       // X midpoints (2i + 1, 2j + 2): columns j0 - 1 .. j0 + TS - 1
   __shared__ Ang MY[kTS][kTS];           // Y midpoints (2i + 2, 2j + 1): columns j0 .. j0 + TS - 1
@@ -296,35 +305,34 @@ __global__ void __launch_bounds__(kTS * kTS, 4) rot_chainrule_kernel(const doubl
   const double* Eb = E + fb * 4 * N;
   double* G = Gf + (long long)b * 2 * NN;
   // left tile: pixel (i, j)
-  chain_pixel(Xf, Yf, Eb, N, C[ti][tj + 1], C[ti][tj + 2], C[ti + 1][tj + 1], MX[ti][tj + 1], MY[ti][tj],
-              G + (long long)i * N + j, NN);
+  double xs = chain_pixel(Xf, Yf, Eb, N, C[ti][tj + 1], C[ti][tj + 2], C[ti + 1][tj + 1], MX[ti][tj + 1],
+                          MY[ti][tj], G + (long long)i * N + j, NN);
   if (pair) {   // mirror tile: pixel (i, N - 1 - j); its phi neighbour / X midpoint mirror column j - 1
-    chain_pixel(Xf, Yf, Eb, N, mirror(C[ti][tj + 1]), mirror(C[ti][tj]), mirror(C[ti + 1][tj + 1]),
-                mirror(MX[ti][tj]), mirror(MY[ti][tj]), G + (long long)i * N + (N - 1 - j), NN);
+    xs += chain_pixel(Xf, Yf, Eb, N, mirror(C[ti][tj + 1]), mirror(C[ti][tj]), mirror(C[ti + 1][tj + 1]),
+                      mirror(MX[ti][tj]), mirror(MY[ti][tj]), G + (long long)i * N + (N - 1 - j), NN);
   }
+  // the closure's row sums (R27), one partial per (map, row, tile pair) in a fixed order: the TS
+  // threads of a row are an aligned group of TS lanes
+  for (int o = TS >> 1; o > 0; o >>= 1) xs += __shfl_xor_sync(__activemask(), xs, o);
+  if (tj == 0) part[((long long)b * N + i) * tcols + (blockIdx.x % tcols)] = xs;
 }
 
-// closure: rows of X_g sum to 0 (subtract the row mean).  One CTA per map, a warp per row.
-__global__ void rot_closure_kernel(double* __restrict__ Gf, int n) {
-  const int N = 1 << n;
-  const long long NN = 1ll << (2 * n);
-  double* X = Gf + (long long)blockIdx.x * 2 * NN;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = warp; r < N; r += nw) {
-    double sx = 0.0;
-    for (int t = lane; t < N; t += 32) sx += X[r * N + t];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    const double mx = sx / (double)N;
-    for (int t = lane; t < N; t += 32) X[r * N + t] -= mx;
-  }
+// the closure's row mean of X_g row r (rows of X sum to zero in the Haar fields, R27)
+__device__ __forceinline__ double row_mean(const double* __restrict__ part, long long b, int N, int tcols, int r) {
+  const double* p = part + ((long long)b * N + r) * tcols;
+  double s = 0.0;
+  for (int c = 0; c < tcols; ++c) s += p[c];
+  return s / (double)N;
 }
 
 // ------------------------------------------------------------------------------- (3) bottom-up
 // from fields at level l+1 (src: [map][planes][4^(l+1)]; at the finest level planes = 2 and
 // Z = X[i] - X[i+1]) to level l (dst [map][3][4^l]) and the level-l details of the output pyramid.
+// part != nullptr (the first level, src = the chain rule's X_g, Y_g): X_g rows corrected by the
+// closure's row means on load.
 __global__ void rot_bottomup_kernel(const double* __restrict__ src, int src_planes, long long maps, int l,
-                                    double* __restrict__ dst, float* __restrict__ out, int n) {
+                                    double* __restrict__ dst, float* __restrict__ out, int n,
+                                    const double* __restrict__ part, int tcols) {
   const int g = 1 << l, G2 = 2 * g;
   const long long per = 1ll << (2 * l), sper = 4 * per;
   const long long total = maps * per;
@@ -340,10 +348,15 @@ __global__ void rot_bottomup_kernel(const double* __restrict__ src, int src_plan
     const double* Y = X + sper;
     const int rr[4] = {2 * i, 2 * i + 1, (2 * i + 2) & (G2 - 1), (2 * i + 3) & (G2 - 1)};
     const int cc[3] = {2 * j, 2 * j + 1, (2 * j + 2) & (G2 - 1)};
-    auto x = [&](int u, int w) { return X[rr[u] * G2 + cc[w]]; };
+    double mr[4] = {0.0, 0.0, 0.0, 0.0};
+    if (part) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) mr[u] = row_mean(part, b, G2, tcols, rr[u]);
+    }
+    auto x = [&](int u, int w) { return X[rr[u] * G2 + cc[w]] - mr[u]; };
     auto y = [&](int u, int w) { return Y[rr[u] * G2 + cc[w]]; };
     auto z = [&](int u, int w) {
-      return zfromx ? X[rr[u] * G2 + cc[w]] - X[rr[u + 1] * G2 + cc[w]] : X[2 * sper + rr[u] * G2 + cc[w]];
+      return zfromx ? x(u, w) - x(u + 1, w) : X[2 * sper + rr[u] * G2 + cc[w]];
     };
     const double Xn = q * (x(0, 0) + 2.0 * x(0, 1) + x(0, 2) + x(1, 0) + 2.0 * x(1, 1) + x(1, 2));
     const double Yn = q * (y(0, 0) + 2.0 * y(1, 0) + y(2, 0) + y(0, 1) + 2.0 * y(1, 1) + y(2, 1));
@@ -357,6 +370,66 @@ __global__ void rot_bottomup_kernel(const double* __restrict__ src, int src_plan
     o[per + cell] = (float)(q * (x(0, 0) + x(1, 0)) * osc);   // one rounding per output
     o[2 * per + cell] = (float)(q * (y(0, 0) + y(0, 1)) * osc);
     o[3 * per + cell] = (float)(q * z(0, 0) * osc);
+  }
+}
+
+
+// Levels ltop-1 .. 0 of one map in shared memory (the per-level kernel's arithmetic, one launch per
+// map instead of one per level): src = the level-ltop fields (2 planes + the closure's partial row
+// sums when ltop = n, straight from the chain rule; else 3 planes).  ltop <= kTailTop.
+constexpr int kTailTop = 5;
+__global__ void __launch_bounds__(256) rot_tail_kernel(const double* __restrict__ src, int src_planes, int ltop,
+                                                       float* __restrict__ out, int n, const double* __restrict__ part,
+                                                       int tcols) {
+  __shared__ double A[3][1 << (2 * kTailTop)];
+  __shared__ double Bf[3][1 << (2 * (kTailTop - 1))];
+  const long long b = blockIdx.x;
+  const int G = 1 << ltop;
+  const int sper = G * G;
+  const long long NN = 1ll << (2 * n);
+  const double* X = src + b * src_planes * (long long)sper;
+  for (int e = threadIdx.x; e < sper; e += blockDim.x) {
+    const int r = e >> ltop;
+    A[0][e] = part ? X[e] - row_mean(part, b, G, tcols, r) : X[e];
+    A[1][e] = X[sper + e];
+    if (src_planes == 3) A[2][e] = X[2 * sper + e];
+  }
+  __syncthreads();
+  if (src_planes == 2) {   // Z = X[i] - X[i + 1] of the (corrected) finest X
+    for (int e = threadIdx.x; e < sper; e += blockDim.x) {
+      const int r = e >> ltop, c = e & (G - 1);
+      A[2][e] = A[0][e] - A[0][((r + 1) & (G - 1)) * G + c];
+    }
+    __syncthreads();
+  }
+  float* o = out + b * NN;
+  for (int l = ltop - 1; l >= 0; --l) {
+    const int g = 1 << l, G2 = 2 * g;
+    const int per = g * g;
+    const double q = 0.25, osc = (double)pow2f(-l);
+    double* dX = ((ltop - 1 - l) & 1) ? &A[0][0] : &Bf[0][0];   // ping-pong: level l into Bf or A
+    const int dstride = ((ltop - 1 - l) & 1) ? (1 << (2 * kTailTop)) : (1 << (2 * (kTailTop - 1)));
+    const double* sX = ((ltop - 1 - l) & 1) ? &Bf[0][0] : &A[0][0];
+    const int sstride = ((ltop - 1 - l) & 1) ? (1 << (2 * (kTailTop - 1))) : (1 << (2 * kTailTop));
+    for (int cell = threadIdx.x; cell < per; cell += blockDim.x) {
+      const int i = cell >> l, j = cell & (g - 1);
+      const int rr[4] = {2 * i, 2 * i + 1, (2 * i + 2) & (G2 - 1), (2 * i + 3) & (G2 - 1)};
+      const int cc[3] = {2 * j, 2 * j + 1, (2 * j + 2) & (G2 - 1)};
+      auto x = [&](int u, int w) { return sX[rr[u] * G2 + cc[w]]; };
+      auto y = [&](int u, int w) { return sX[sstride + rr[u] * G2 + cc[w]]; };
+      auto z = [&](int u, int w) { return sX[2 * sstride + rr[u] * G2 + cc[w]]; };
+      const double Xn = q * (x(0, 0) + 2.0 * x(0, 1) + x(0, 2) + x(1, 0) + 2.0 * x(1, 1) + x(1, 2));
+      const double Yn = q * (y(0, 0) + 2.0 * y(1, 0) + y(2, 0) + y(0, 1) + 2.0 * y(1, 1) + y(2, 1));
+      const double Zn = q * ((z(0, 0) + 2.0 * z(0, 1) + z(0, 2)) + 2.0 * (z(1, 0) + 2.0 * z(1, 1) + z(1, 2)) +
+                            (z(2, 0) + 2.0 * z(2, 1) + z(2, 2)));
+      dX[cell] = Xn;
+      dX[dstride + cell] = Yn;
+      dX[2 * dstride + cell] = Zn;
+      o[per + cell] = (float)(q * (x(0, 0) + x(1, 0)) * osc);
+      o[2 * per + cell] = (float)(q * (y(0, 0) + y(0, 1)) * osc);
+      o[3 * per + cell] = (float)(q * z(0, 0) * osc);
+    }
+    __syncthreads();
   }
 }
 
@@ -394,23 +467,29 @@ __global__ void __launch_bounds__(256) rot_dc_kernel(const float* __restrict__ i
   const int N = 1 << n;
   const double ca = prm.ca[map0 + b], sa = prm.sa[map0 + b];
   float acc = 0.f;
-  for (long long p = threadIdx.x; p < NN; p += blockDim.x) {
-    const int i = (int)(p >> n), j = (int)(p & (N - 1));
-    float jT, jP;
-    rotated_kf(tr, 2 * i + 1, 2 * j + 1, (float)ca, (float)sa, jT, jP);
+  const float* P = A[cb];
+  auto sample = [&](float jT, float jP) {
     const float y = jT * (float)M / 3.14159265358979f - 0.5f;   // in [-1/2, M - 1/2]
     const float x = jP * (float)M / 6.283185307179586f - 0.5f;
     const float fy = floorf(y), fx = floorf(x);
     const float wy = y - fy, wx = x - fx;
-    const float* P = A[cb];
     auto at = [&](int r, int c) {  // rows beyond a pole: the pole row seen from phi + pi
       if (r < 0) { r = -1 - r; c += M / 2; }
       if (r >= M) { r = 2 * M - 1 - r; c += M / 2; }
       return P[r * M + (c & (M - 1))];
     };
     const int y0 = (int)fy, x0 = (int)fx;
-    acc += (1.f - wy) * ((1.f - wx) * at(y0, x0) + wx * at(y0, x0 + 1)) +
+    return (1.f - wy) * ((1.f - wx) * at(y0, x0) + wx * at(y0, x0 + 1)) +
            wy * ((1.f - wx) * at(y0 + 1, x0) + wx * at(y0 + 1, x0 + 1));
+  };
+  // pixel (i, j) and its mirror (i, N - 1 - j) about phi = pi: Phi -> 2 pi - Phi (as the chain rule)
+  const int hN = N / 2;
+  for (long long p = threadIdx.x; p < NN / 2; p += blockDim.x) {
+    const int i = (int)(p / hN), j = (int)(p - (long long)i * hN);
+    float jT, jP;
+    rotated_kf(tr, 2 * i + 1, 2 * j + 1, (float)ca, (float)sa, jT, jP);
+    acc += sample(jT, jP);
+    acc += sample(jT, jP == 0.f ? 0.f : 6.283185307179586f - jP);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -431,6 +510,9 @@ unsigned grid_for(long long total) {
 
 }  // namespace
 
+// tile pairs per row of the chain rule = the closure's partial row sums per row
+int closure_cols(int n) { return (1 << n) >= 2 * kTS ? (1 << n) / (2 * kTS) : 1; }
+
 // Workspace (fp64 fields: fp32 rounding of the fine differences is amplified on the coarse levels
 // the recursion sums): F ping-pong 2 x [chunk][2][N^2] doubles, G [chunk][2][N^2]
 // doubles, pole rows [chunk][4][N] doubles, the trig table, the pre-azimuth pyramids [maps][N^2]
@@ -442,7 +524,8 @@ size_t rotate_workspace_bytes_impl(int log2n, long long maps) {
   const size_t pb = (mc * 4 * ((size_t)1 << log2n) * sizeof(double) + 255) & ~size_t(255);
   const size_t tb = (4 * (2 * ((size_t)1 << log2n) + 2) * sizeof(double) + 255) & ~size_t(255);
   const size_t tp = ((size_t)maps * NN * sizeof(float) + 255) & ~size_t(255);
-  return 3 * fd + pb + tb + tp + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
+  const size_t pr = (mc * ((size_t)1 << log2n) * (size_t)closure_cols(log2n) * sizeof(double) + 255) & ~size_t(255);
+  return 3 * fd + pb + tb + tp + pr + ((shift_workspace_bytes_impl(2, log2n, maps) + 255) & ~size_t(255));
 }
 
 hs_status launch_rotate(const float* in, float* out, int n, long long maps, const double* angles, void* ws,
@@ -461,8 +544,11 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
   double* poles = reinterpret_cast<double*>(base + 3 * fd);
   double* tab = reinterpret_cast<double*>(base + 3 * fd + pb);
   float* tmp = reinterpret_cast<float*>(base + 3 * fd + pb + tb);
-  void* sws = base + 3 * fd + pb + tb + tp;
-  const size_t sws_bytes = ws_bytes - (3 * fd + pb + tb + tp);
+  const int tcols = closure_cols(n);
+  const size_t pr = (mcap * ((size_t)1 << n) * (size_t)tcols * sizeof(double) + 255) & ~size_t(255);
+  double* part = reinterpret_cast<double*>(base + 3 * fd + pb + tb + tp);
+  void* sws = base + 3 * fd + pb + tb + tp + pr;
+  const size_t sws_bytes = ws_bytes - (3 * fd + pb + tb + tp + pr);
   rot_table_kernel<<<(K + 255) / 256, 256, 0, st>>>(n, tab);
   HS_CHECK_LAUNCH("rot_table_kernel");
   const Trig tr{tab, tab + K, tab + 2 * K, tab + 3 * K};
@@ -493,21 +579,31 @@ hs_status launch_rotate(const float* in, float* out, int n, long long maps, cons
       const int TS = (1 << n) < kTS ? (1 << n) : kTS;
       const int tpr = (1 << n) / TS;
       const int ctas = (tpr >= 2 ? tpr / 2 : 1) * tpr;   // tile pairs (mirror about phi = pi)
-      rot_chainrule_kernel<<<dim3(ctas, (unsigned)mc), kTS * kTS, 0, st>>>(cur, poles, n, prm, tr, Gf, bcast ? 0 : 1);
+      rot_chainrule_kernel<<<dim3(ctas, (unsigned)mc), kTS * kTS, 0, st>>>(cur, poles, n, prm, tr, Gf, bcast ? 0 : 1,
+                                                                           part);
     }
     HS_CHECK_LAUNCH("rot_chainrule_kernel");
-    rot_closure_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, n);
-    HS_CHECK_LAUNCH("rot_closure_kernel");
-    // (3) bottom-up, every detail level of the rotated pyramid
-    const double* s = Gf;
-    int planes = 2;
-    double* d = bufA;
-    for (int l = n - 1; l >= 0; --l) {
-      rot_bottomup_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(s, planes, mc, l, d, dtmp, n);
-      HS_CHECK_LAUNCH("rot_bottomup_kernel");
-      s = d;
-      planes = 3;
-      d = (d == bufA) ? bufB : bufA;
+    // (3) bottom-up, every detail level of the rotated pyramid; the closure (R27) is applied as
+    // the first level loads X_g (row means from the chain rule's partial sums); levels below
+    // kTailTop in one launch per chunk
+    if (n <= kTailTop) {
+      rot_tail_kernel<<<(unsigned)mc, 256, 0, st>>>(Gf, 2, n, dtmp, n, part, tcols);
+      HS_CHECK_LAUNCH("rot_tail_kernel");
+    } else {
+      const double* s = Gf;
+      int planes = 2;
+      double* d = bufA;
+      const double* pp = part;
+      for (int l = n - 1; l >= kTailTop; --l) {
+        rot_bottomup_kernel<<<grid_for(mc << (2 * l)), 256, 0, st>>>(s, planes, mc, l, d, dtmp, n, pp, tcols);
+        HS_CHECK_LAUNCH("rot_bottomup_kernel");
+        pp = nullptr;
+        s = d;
+        planes = 3;
+        d = (d == bufA) ? bufB : bufA;
+      }
+      rot_tail_kernel<<<(unsigned)mc, 256, 0, st>>>(s, 3, kTailTop, dtmp, n, nullptr, 0);
+      HS_CHECK_LAUNCH("rot_tail_kernel");
     }
     rot_dc_kernel<<<(unsigned)mc, 256, 0, st>>>(src, bcast ? 0 : NN, n, 0, prm, tr, dtmp);
     HS_CHECK_LAUNCH("rot_dc_kernel");

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
   extern __shared__ __align__(16) double smem[];
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
-  const int n = args.log2n, N = 1 << n;
+  const int n = args.log2n;
   const int m = P.m;
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
@@ -57,7 +57,6 @@ __global__ void __launch_bounds__(k1DThreads) shift1d_kernel(const __grid_consta
     out[idx] = in[(1 << l) + sk];
   }
   if (m == 0) return;
-  (void)N;
   if ((reinterpret_cast<unsigned long long>(in) & 15) == 0 && gm >= 4) {
     for (int idx = threadIdx.x; idx < gm / 4; idx += blockDim.x)
       reinterpret_cast<float4*>(S)[idx] = __ldg(reinterpret_cast<const float4*>(in) + idx);

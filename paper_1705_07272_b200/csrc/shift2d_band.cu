@@ -51,9 +51,6 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
-}
 
 // Band geometry at working level M.  Level l in [L, M) (L = M - 4): the band reads the detail rows
 // [Slo >> (M - l), Shi >> (M - l)] -- exactly NR(l) = (kBH >> (M - l)) + 1 rows of 2^l columns (the
