@@ -153,6 +153,63 @@ __device__ __forceinline__ void topdown_last(const double* __restrict__ P, int p
   }
 }
 
+// Stage level l's detail rows (NR(l) rows from Slo >> (M - l), 3 planes) -- compile-time l, so
+// every index division is by a constant.
+template <int M, int l>
+__device__ __forceinline__ void stage_level(const float* __restrict__ in, int Slo, bool al16, float* __restrict__ stage) {
+  using G = BG<M>;
+  constexpr int gl = 1 << l, nr = G::NR(l);
+  constexpr long long per = 1ll << (2 * l);
+  const int llo = Slo >> (M - l);
+  float* S = stage + G::SOFF(l);
+  if (al16 && l >= 2) {
+    constexpr int q = gl / 4;                       // 16-byte chunks per row
+    for (int idx = threadIdx.x; idx < 3 * nr * q; idx += kBandThreads) {
+      const int row = idx / q, c4 = idx - row * q;   // row = t * nr + rr
+      const int t = row / nr, rr = row - t * nr;
+      cp_async16(S + row * gl + 4 * c4, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + 4 * c4);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < 3 * nr * gl; idx += kBandThreads) {
+      const int row = idx >> l, c = idx & (gl - 1);
+      const int t = row / nr, rr = row - t * nr;
+      cp_async4(S + idx, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + c);
+    }
+  }
+  if constexpr (l + 1 < M - 1) stage_level<M, l + 1>(in, Slo, al16, stage);
+}
+
+// Levels l .. L-1 of the top-down on one warp (two parent rows per level, at most 2 x 2^(L-1)
+// parents: warp-synchronous, no block barrier); returns the first stored row of level L.
+template <int M, int l>
+__device__ __forceinline__ int coarse_levels(const float* __restrict__ stage, int Slo, int base, double* cur,
+                                             double* nxt) {
+  using G = BG<M>;
+  constexpr int L = G::L;
+  if constexpr (l == L) {
+    return base;
+  } else {
+    constexpr int gl = 1 << l;
+    constexpr float asc = float(1u << l);
+    const int lane = threadIdx.x & 31;
+    const int lo = Slo >> (M - l);
+    const float* S = stage + G::SOFF(l);
+    for (int idx = lane; idx < 2 * gl; idx += 32) {
+      const int rr = idx >> l, j = idx & (gl - 1);
+      const double a = cur[(lo + rr - base) * gl + j];
+      const double H = (double)(S[idx] * asc), V = (double)(S[2 * gl + idx] * asc), D = (double)(S[4 * gl + idx] * asc);
+      const double p = a + V, q = a - V, sm = H + D, t = H - D;
+      double* c0 = nxt + (2 * rr) * (2 * gl) + 2 * j;
+      c0[0] = p + sm;
+      c0[1] = p - sm;
+      c0[2 * gl] = q + t;
+      c0[2 * gl + 1] = q - t;
+    }
+    __syncwarp();
+    return coarse_levels<M, l + 1>(stage, Slo, 2 * lo, nxt, cur);
+  }
+}
+
 template <int M>
 __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam& P, int g, double* smem) {
   using G = BG<M>;
@@ -194,59 +251,19 @@ __device__ __forceinline__ void band_cta(const ShiftArgs& args, const FaceParam&
   // levels 0 .. M-2 -> shared memory (cp.async)
   {
     const bool al16 = ((reinterpret_cast<unsigned long long>(in) & 15) == 0);
-#pragma unroll
-    for (int l = 0; l < M - 1; ++l) {
-      const int gl = 1 << l, nr = G::NR(l);
-      const int llo = Slo >> (M - l);
-      const long long per = 1ll << (2 * l);
-      float* S = stage + G::SOFF(l);
-      if (al16 && l >= 2) {
-        const int q = gl / 4;                       // 16-byte chunks per row
-        for (int idx = tid; idx < 3 * nr * q; idx += kBandThreads) {
-          const int row = idx / q, c4 = idx - row * q;   // row = t * nr + rr
-          const int t = row / nr, rr = row - t * nr;
-          cp_async16(S + row * gl + 4 * c4, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + 4 * c4);
-        }
-      } else {
-        for (int idx = tid; idx < 3 * nr * gl; idx += kBandThreads) {
-          const int row = idx >> l, c = idx & (gl - 1);
-          const int t = row / nr, rr = row - t * nr;
-          cp_async4(S + idx, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + c);
-        }
-      }
-    }
+    stage_level<M, 0>(in, Slo, al16, stage);
     if (tid < 2) sC[tid] = 0.0;                      // A_0 = 0 (rows lo_0, lo_0 + 1 of level 0)
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
   }
 
   // ------------------------------------------------------------------ top-down 0 -> M
-  // levels 0 .. L-1: two parent rows from lo_l each (one or both needed), ping-pong in sC
-  double* cur = sC;                                  // level l rows from base_l
-  double* nxt = sC + 4 * WL;
-  int base = Slo >> M;                               // A_0: rows base, base + 1 (both 0)
-#pragma unroll 1
-  for (int l = 0; l < L; ++l) {
-    const int gl = 1 << l, lo = Slo >> (M - l);
-    const double asc = p2d(l);
-    const float* S = stage + G::SOFF(l);
-    for (int idx = tid; idx < 2 * gl; idx += kBandThreads) {
-      const int rr = idx >> l, j = idx & (gl - 1);
-      const double a = cur[(lo + rr - base) * gl + j];
-      const double H = (double)S[idx] * asc, V = (double)S[2 * gl + idx] * asc, D = (double)S[4 * gl + idx] * asc;
-      const double p = a + V, q = a - V, sm = H + D, t = H - D;
-      double* c0 = nxt + (2 * rr) * (2 * gl) + 2 * j;
-      c0[0] = p + sm;
-      c0[1] = p - sm;
-      c0[2 * gl] = q + t;
-      c0[2 * gl + 1] = q - t;
-    }
-    __syncthreads();
-    base = 2 * lo;
-    double* t = cur;
-    cur = nxt;
-    nxt = t;
-  }
+  // levels 0 .. L-1 on warp 0 (two parent rows from lo_l each, ping-pong in sC); A_0 = 0
+  double* const cL = (L & 1) ? sC + 4 * WL : sC;      // where level L lands after L ping-pongs
+  if (tid < 32) coarse_levels<M, 0>(stage, Slo, Slo >> M, sC, sC + 4 * WL);
+  const int base = 2 * (Slo >> (M - L + 1));          // level L's first stored row (2 lo_{L-1})
+  __syncthreads();
+  double* cur = cL;
   // levels L .. M-1 (exact row counts)
   const int lo0 = Slo >> 4, lo1 = Slo >> 3, lo2 = Slo >> 2, lo3 = Slo >> 1;
   topdown_step<L, G::NR(L)>(cur, base, lo0, stage + G::SOFF(L), bufB);
