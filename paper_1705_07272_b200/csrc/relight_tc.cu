@@ -59,7 +59,7 @@ constexpr uint32_t ACC_COL0 = ASTAGES * 64;  // 256
 // One CTA per frame: per-frame power-of-2 scale s_b (max |L_b s_b| in [2^14, 2^15)), then the
 // fp16 hi/lo split of L_b s_b written into pre-swizzled 16 KB tiles [L_hi 64 rows | L_lo 64 rows]
 // per (frame block, k block) -- exactly the 128B-swizzled K-major smem image the MMA reads.
-__global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __restrict__ L, long long lstride,
+__global__ void __launch_bounds__(1024) relight_tc_prep_kernel(const float* __restrict__ L, long long lstride,
                                                                int faces, int kshift, int K, uint8_t* __restrict__ tiles,
                                                                float* __restrict__ inv_scale, RedoList* __restrict__ redo) {
   const int b = blockIdx.x;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) relight_tc_prep_kernel(const float* __res
   const int fb = b / BN, r = b % BN;
   const int kmask = (1 << kshift) - 1;
   const float* Lb = L + (long long)b * faces * lstride;
-  __shared__ float red[8];
+  __shared__ float red[32];
   float mx = 0.f;
   for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(Lb + (long long)(k >> kshift) * lstride + (k & kmask))));
 #pragma unroll
@@ -385,7 +385,7 @@ hs_status launch_relight_tc_prep(const float* L, long long lstride, int faces, i
   uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
   float* inv = reinterpret_cast<float*>(tiles + tc_tiles_bytes(faces, kface, batch));
   RedoList* redo = reinterpret_cast<RedoList*>(tiles + tc_redo_offset(faces, kface, batch));
-  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);
+  relight_tc_prep_kernel<<<batch, 1024, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);   // one CTA per frame: K / 1024 loads per thread
   HS_CHECK_LAUNCH("relight_tc_prep_kernel");
   return HS_OK;
 }
@@ -419,7 +419,7 @@ hs_status launch_relight_tc(const float* T, long long V, int faces, int kface, c
   }
   HS_SMEM_ATTR(relight_tc_kernel, SMEM_BYTES);
 
-  relight_tc_prep_kernel<<<batch, 256, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);
+  relight_tc_prep_kernel<<<batch, 1024, 0, st>>>(L, lstride, faces, kshift, K, tiles, inv, redo);   // one CTA per frame: K / 1024 loads per thread
   HS_CHECK_LAUNCH("relight_tc_prep_kernel");
   const int ntiles = (int)((V + BM - 1) / BM);
   const long long nwork = (long long)ntiles * (batch / BN);
