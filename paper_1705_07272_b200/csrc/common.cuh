@@ -124,14 +124,14 @@ struct ShiftArgs {
   long long in_face_stride;   // elements between the faces of one batch entry (>= K)
   long long ws_face_stride;   // BYTES per face in ws (ws_face_floats_2d doubles)
   int log2n, faces, band, out_face_stride, num_faces;
-  int stream;                 // 1: faces with kStreamMinLevel <= m <= kStreamMaxLevel go to shift2d_band_kernel
+  int band_path;              // 1: faces with kBandMinLevel <= m <= kBandMaxLevel go to shift2d_band_kernel
   FaceParam fp[kMaxFacesPerLaunch];
 };
 
 // Working levels handled by the band kernel (shift2d_band.cu); max_m: the largest such level present.
-constexpr int kStreamMinLevel = 6;
-constexpr int kStreamMaxLevel = 9;
-inline __host__ __device__ bool stream_level(int m) { return m >= kStreamMinLevel && m <= kStreamMaxLevel; }
+constexpr int kBandMinLevel = 6;
+constexpr int kBandMaxLevel = 9;
+inline __host__ __device__ bool band_level(int m) { return m >= kBandMinLevel && m <= kBandMaxLevel; }
 hs_status launch_shift2d_band(ShiftArgs& a, int max_m, cudaStream_t st);   // shift2d_band.cu
 
 // Tiling constants of the 2D tile kernel.

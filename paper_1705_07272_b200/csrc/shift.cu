@@ -152,14 +152,14 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
     int max_tiles = 0;
     bool any_perm = false, any_coarse = false, any_tile = false;
     int max_band_m = 0;   // largest working level taken by the band kernel (0: none)
-    a.stream = (ndim == 2) ? 1 : 0;
+    a.band_path = (ndim == 2) ? 1 : 0;
     if (shifts_host) {
       for (int i = 0; i < nf; ++i) {
         const double* s = shifts_host + (g0 + i) * ndim;
         a.fp[i] = (ndim == 2) ? make_face_param_2d(s[0], s[1], n) : make_face_param_1d(s[0], n);
         max_tiles = std::max(max_tiles, shift2d_tiles_for(a.fp[i].m));
         if (a.fp[i].m < band || a.fp[i].m == 0) any_perm = true;
-        if (a.stream && stream_level(a.fp[i].m)) {
+        if (a.band_path && band_level(a.fp[i].m)) {
           max_band_m = std::max(max_band_m, a.fp[i].m);
         } else if (a.fp[i].m > 0) {
           any_tile = true;
@@ -178,7 +178,7 @@ hs_status launch_shift(const float* in, float* out, int ndim, int log2n, int fac
       any_perm = true;
       any_coarse = coarse_level(n) > 0;
       any_tile = true;
-      max_band_m = (a.stream && n >= kStreamMinLevel) ? std::min(n, kStreamMaxLevel) : 0;
+      max_band_m = (a.band_path && n >= kBandMinLevel) ? std::min(n, kBandMaxLevel) : 0;
     }
     if (ndim == 2) {
       hs_status s = launch_shift2d(a, max_tiles, any_coarse, any_perm, any_tile, max_band_m, st);

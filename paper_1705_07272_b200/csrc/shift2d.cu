@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(kThreads) coarse_fields_kernel(const __grid_co
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int c = P.m > KF ? P.m - KF : 0;
-  if (c == 0 || (args.stream && stream_level(P.m))) return;   // band faces: shift2d_band_kernel
+  if (c == 0 || (args.band_path && band_level(P.m))) return;   // band faces: shift2d_band_kernel
   const int b = g / args.faces, f = g % args.faces;
   const float* __restrict__ in = args.in + (long long)b * args.in_batch_stride + (long long)f * args.in_face_stride;
   using FT = double;   // always fp64: the coarse recursion carries pixel-value-scale errors otherwise
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kThreads) coarse_finish_kernel(const __grid_co
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int c = P.m > KF ? P.m - KF : 0;
-  if (c == 0 || (args.stream && stream_level(P.m))) return;   // band faces: band_finish_kernel
+  if (c == 0 || (args.band_path && band_level(P.m))) return;   // band faces: band_finish_kernel
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   char* wsb = reinterpret_cast<char*>(args.ws) + (long long)g * args.ws_face_stride;
   FT* wsf = reinterpret_cast<FT*>(wsb);
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(FT) == 4 ? 3 : 2) shift2d_til
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   const int m = P.m;
   if (m == 0) return;  // identity: handled by permute_kernel
-  if (args.stream && stream_level(m)) return;   // shift2d_band_kernel
+  if (args.band_path && band_level(m)) return;   // shift2d_band_kernel
   const int c = m > KF ? m - KF : 0;
   const int k = m - c;
   const int tc = (1 << c) < TC ? (1 << c) : TC;
@@ -883,7 +883,7 @@ hs_status launch_shift2d(ShiftArgs& a, int max_tiles, bool any_coarse, bool any_
     // fp64 fields at every size: fp32 rounding in the difference fields is amplified ~2^(n-l) on a
     // band of level l; the randomised sweep (tests/test_gpu_fuzz.py) measured
     // 2e-5 for white noise at N = 64 with fp32 fields.
-    hs_status s = launch_tiles<double>(a, max_tiles, any_coarse, any_tile, a.stream ? max_band_m : 0, st);
+    hs_status s = launch_tiles<double>(a, max_tiles, any_coarse, any_tile, a.band_path ? max_band_m : 0, st);
     if (s != HS_OK) return s;
   }
   if (any_perm) {

@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kBandThreads) band_finish_kernel(const __grid_
   __shared__ double sA[32 * 32 + 16 * 16];
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
-  if (!stream_level(P.m)) return;
+  if (!band_level(P.m)) return;
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   if (threadIdx.x == 0) {   // scaling coefficient: unchanged (R8)
     const int b_ = g / args.faces, f_ = g % args.faces;
@@ -406,10 +406,10 @@ __global__ void __launch_bounds__(kBandThreads) band_finish_kernel(const __grid_
 
 // grid (bands of the largest working level present, faces); faces at other levels exit at once.
 hs_status launch_shift2d_band(ShiftArgs& a, int max_m, cudaStream_t st) {
-  if (max_m < kStreamMinLevel) return HS_OK;
-  if (max_m > kStreamMaxLevel) max_m = kStreamMaxLevel;
+  if (max_m < kBandMinLevel) return HS_OK;
+  if (max_m > kBandMaxLevel) max_m = kBandMaxLevel;
   const size_t smem = band_smem_bytes(max_m);
-  HS_SMEM_ATTR(shift2d_band_kernel, band_smem_bytes(kStreamMaxLevel));
+  HS_SMEM_ATTR(shift2d_band_kernel, band_smem_bytes(kBandMaxLevel));
   shift2d_band_kernel<<<dim3((1u << max_m) / kBH, a.num_faces), kBandThreads, smem, st>>>(a);
   HS_CHECK_LAUNCH("shift2d_band_kernel");
   band_finish_kernel<<<a.num_faces, kBandThreads, 0, st>>>(a);
