@@ -162,14 +162,19 @@ __device__ __forceinline__ void stage_level(const float* __restrict__ in, int Sl
   constexpr long long per = 1ll << (2 * l);
   const int llo = Slo >> (M - l);
   float* S = stage + G::SOFF(l);
-  if (al16 && l >= 2) {
-    constexpr int q = gl / 4;                       // 16-byte chunks per row
-    for (int idx = threadIdx.x; idx < 3 * nr * q; idx += kBandThreads) {
-      const int row = idx / q, c4 = idx - row * q;   // row = t * nr + rr
-      const int t = row / nr, rr = row - t * nr;
-      cp_async16(S + row * gl + 4 * c4, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + 4 * c4);
+  bool done = false;
+  if constexpr (l >= 2) {
+    if (al16) {
+      constexpr int q = gl / 4;                     // 16-byte chunks per row
+      for (int idx = threadIdx.x; idx < 3 * nr * q; idx += kBandThreads) {
+        const int row = idx / q, c4 = idx - row * q;   // row = t * nr + rr
+        const int t = row / nr, rr = row - t * nr;
+        cp_async16(S + row * gl + 4 * c4, in + per * (1 + t) + (long long)((llo + rr) & (gl - 1)) * gl + 4 * c4);
+      }
+      done = true;
     }
-  } else {
+  }
+  if (!done) {
     for (int idx = threadIdx.x; idx < 3 * nr * gl; idx += kBandThreads) {
       const int row = idx >> l, c = idx & (gl - 1);
       const int t = row / nr, rr = row - t * nr;
