@@ -116,3 +116,17 @@ def test_accuracy_against_the_spatial_rotation():
         assert abs(e_gpu - e_alg) <= 1e-5 * max(1.0, e_alg) + 1e-6
         errs.append(e_gpu)
     assert errs[1] < errs[0]
+
+
+def test_composed_edge_normals_and_full_band():
+    """normals at the poles, on the equator at phi = 0 and pi, and just inside the 2 pi seam; the
+    band equal to the whole map (log2k = log2n); 130 vertices (a ragged 128-row tile)"""
+    n = k = 4
+    brdf, vis, light, nrm = _case(1705, n, k, 130, 64)
+    edge = np.array([[0.0, 0.0], [np.pi, 0.0], [np.pi / 2, 0.0], [np.pi / 2, np.pi], [1e-9, 2 * np.pi - 1e-9],
+                     [np.pi - 1e-9, 1e-9], [np.pi / 4, 3 * np.pi / 2]])
+    nrm[:len(edge)] = edge
+    got = _gpu(brdf, vis, light, nrm, k)
+    ref = _reference(brdf, vis, light, nrm, k, orot.rotate_coeffs_chain)
+    assert _rel(got, ref) <= 1e-5
+    assert _rel(got[:len(edge)], ref[:len(edge)]) <= 1e-5
