@@ -260,3 +260,26 @@ def test_shift_largest_faces(n, band, sh):
     ref = oshift.shift_coeffs(c, np.array([[list(sh)]]), 2, band_levels=band)
     err = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
     assert err <= 1e-5, (n, band, err)
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_relight_shifted_large_faces(case):
+    """Per-vertex shifts at N = 256 and 512: the chunked path (a batched shift of the vertex chunk
+    with classifications computed on the device, then the row dot) -- the band kernel and the tile
+    kernel on device-side FaceParams, every shift class mixed in one chunk."""
+    import torch
+    import paper_1705_07272_b200 as hs
+    rng = np.random.default_rng(9000 + case)
+    n = 8 if case < 2 else 9
+    N = 1 << n
+    faces = 2 if n == 8 else 1
+    V = 24
+    L = synth.light_pyramids(900 + case, 1, faces, n)[0]
+    T = synth.transfer_rows(900 + case, int(rng.integers(0, 10 ** 6)), V, faces, N * N)
+    vs = np.array([[_shift_value(rng, N), _shift_value(rng, N)] for _ in range(V)], dtype=np.float32)
+    vs[:4] = [[0, 0], [N / 2, 8], [3, 0.5], [64, 128]]
+    got = hs.relight_vertices_shifted(torch.from_numpy(T).cuda(), torch.from_numpy(L).cuda(),
+                                      torch.from_numpy(vs).cuda()).cpu().numpy()
+    ref = orelight.relight_shifted(T, L, vs.astype(np.float64))
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 1e-5, (n, faces, V, err)
