@@ -71,6 +71,24 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+# fp64 ALU roofline of the rotation (row f1): peak = 148 SMs x 64 fp64 FMA per clock
+# (one warp DFMA per 2 cycles per SMSP, consistent with ncu's fp64-pipe counters on the shift
+# kernels) x 2 flops x the max SM clock; the algorithmic count per rotated pixel: the chain rule
+# (1.63 rotated samples x ~63 flops: the rotation, |(x', z')| and two atan2; 2 output differences x
+# ~31 flops: two bilinear field samples and the increments) plus the bottom-up (~20 per pixel).
+ROT_FP64_FLOPS_PER_PIXEL = 185
+
+
+def fp64_peak_tflops():
+    mhz = 1965.0
+    try:
+        with open(PEAKS_PATH) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    except (OSError, ValueError):
+        pass
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12, f"derived: 148 SMs x 64 fp64 FMA/clk x 2 x {mhz:.0f} MHz (DESIGN.md §5.9)"
+
+
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons polled through NVML every ~2 ms on a background
     thread; ``mark(True/False)`` brackets the timed region and ``summary()`` reports the samples
@@ -1037,12 +1055,16 @@ def run_rotate(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "N": N, "maps": B, "l2": "inputs 67 MB < L2; no flush"},
         "rotated_coeffs_per_sec": B * NN / (ms * 1e-3),
-        "roofline": {"bound": "hbm", "kernel": "haar_rotate_coeffs (all launches)",
-                     "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": peak_src,
-                     "unit": "GB/s", "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None,
-                     "alg_bytes_per_launch": alg, "avg_launch_ms": ms, "share_of_step": 1.0,
-                     "note": "staged multi-launch path (fields in the workspace); bound by the per-sample "
-                             "trigonometry of the chain-rule kernel (SFU/ALU), not by HBM"},
+        "roofline": {"bound": "alu", "kernel": "haar_rotate_coeffs (all launches)",
+                     "achieved": B * NN * ROT_FP64_FLOPS_PER_PIXEL / (ms * 1e-3) / 1e12, "peak": fp64_peak_tflops()[0],
+                     "peak_source": fp64_peak_tflops()[1], "unit": "TFLOP/s",
+                     "frac": B * NN * ROT_FP64_FLOPS_PER_PIXEL / (ms * 1e-3) / 1e12 / fp64_peak_tflops()[0],
+                     "traffic": None, "alg_flops_per_launch": B * NN * ROT_FP64_FLOPS_PER_PIXEL,
+                     "avg_launch_ms": ms, "share_of_step": 1.0,
+                     "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_launch": alg,
+                     "note": "fp64 operations of the method (chain rule + bottom-up) against the fp64 FMA peak; the "
+                             "chain-rule kernel is issue / latency bound (trigonometry, bilinear samples), the fp64 "
+                             "pipe ~25-35 % busy"},
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": None,
     }
     if not args.no_e2e:
@@ -1200,11 +1222,14 @@ def run_shade(args, cfg):
         "config": {"workload": f"{cfg.name}: {cfg.note}", "faces": 1, "N": N, "frames": B, "vertices": V,
                    "k_face": kf, "l2": "no flush"},
         "roofline": {"bound": "alu", "kernel": "relight_vertices_brdf_rotated (rotation + pack + triple product)",
-                     "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None, "alg_bytes_per_launch": alg,
+                     "achieved": V * N * N * ROT_FP64_FLOPS_PER_PIXEL / (ms * 1e-3) / 1e12,
+                     "peak": fp64_peak_tflops()[0], "peak_source": fp64_peak_tflops()[1], "unit": "TFLOP/s",
+                     "frac": V * N * N * ROT_FP64_FLOPS_PER_PIXEL / (ms * 1e-3) / 1e12 / fp64_peak_tflops()[0],
+                     "traffic": None, "alg_flops_per_launch": V * N * N * ROT_FP64_FLOPS_PER_PIXEL,
                      "avg_launch_ms": ms, "share_of_step": 1.0,
-                     "note": "reported against HBM for scale; the per-vertex rotation's fp64 chain rule (acos / "
-                             "atan2 per rotated sample) bounds the call, as in c6r"},
+                     "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_launch": alg,
+                     "note": "the per-vertex BRDF rotation's fp64 operations (as c6r) against the fp64 FMA peak; the "
+                             "triple product and the pack are a few % of the call"},
         "gpu_launches": launches["n"], "clocks": clk.summary(), "e2e": e2e,
     }
     if not args.no_cpu_baseline:
