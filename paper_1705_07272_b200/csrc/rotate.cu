@@ -281,19 +281,29 @@ __global__ void __launch_bounds__(kTS * kTS, 4) rot_chainrule_kernel(const doubl
   const double ca = prm.ca[b], sa = prm.sa[b];
   const int nt = TS * TS;
   const int K2 = 2 * N;                            // half-step column index modulo 2N
-  for (int k = threadIdx.x; k < (TS + 1) * (TS + 2); k += blockDim.x) {
-    const int r = k / (TS + 2), c = k - r * (TS + 2) - 1;   // c = -1 .. TS
-    const int kp = (2 * (j0 + c) + 1 + K2) % K2;
-    C[r][c + 1] = rotated_k(tr, 2 * (i0 + r) + 1, kp, ca, sa);
-  }
-  for (int k = threadIdx.x; k < TS * (TS + 1); k += blockDim.x) {
-    const int r = k / (TS + 1), c = k - r * (TS + 1) - 1;   // c = -1 .. TS - 1
-    const int kp = (2 * (j0 + c) + 2 + K2) % K2;
-    MX[r][c + 1] = rotated_k(tr, 2 * (i0 + r) + 1, kp, ca, sa);
-  }
-  for (int k = threadIdx.x; k < TS * TS; k += blockDim.x) {
-    const int r = k / TS, c = k - r * TS;
-    MY[r][c] = rotated_k(tr, 2 * (i0 + r) + 2, 2 * (j0 + c) + 1, ca, sa);
+  // one flat index space over the three angle grids (the block's threads share the 834 rotations
+  // evenly: separate loops left the first threads of each grid a rotation more than the rest)
+  const int nC = (TS + 1) * (TS + 2), nX = TS * (TS + 1), nY = TS * TS;
+  for (int k = threadIdx.x; k < nC + nX + nY; k += blockDim.x) {
+    int kt, kp;
+    Ang* dst;
+    if (k < nC) {
+      const int r = k / (TS + 2), c = k - r * (TS + 2) - 1;   // c = -1 .. TS
+      kt = 2 * (i0 + r) + 1;
+      kp = (2 * (j0 + c) + 1 + K2) % K2;
+      dst = &C[r][c + 1];
+    } else if (k < nC + nX) {
+      const int e = k - nC, r = e / (TS + 1), c = e - r * (TS + 1) - 1;   // c = -1 .. TS - 1
+      kt = 2 * (i0 + r) + 1;
+      kp = (2 * (j0 + c) + 2 + K2) % K2;
+      dst = &MX[r][c + 1];
+    } else {
+      const int e = k - nC - nX, r = e / TS, c = e - r * TS;
+      kt = 2 * (i0 + r) + 2;
+      kp = 2 * (j0 + c) + 1;
+      dst = &MY[r][c];
+    }
+    *dst = rotated_k(tr, kt, kp, ca, sa);
   }
   __syncthreads();
   if (threadIdx.x >= nt) return;
