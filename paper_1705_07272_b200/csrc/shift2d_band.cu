@@ -363,6 +363,9 @@ __global__ void __launch_bounds__(kBandThreads, 4) shift2d_band_kernel(const __g
     case 9: band_cta<9>(args, P, g, smem); break;
     default: break;
   }
+  // programmatic dependent launch: band_finish_kernel may be scheduled once every band CTA got
+  // here (it waits for this grid's completion and memory before reading the workspace)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Levels m-5 .. 0 of one face from A'_{m-4} (the bands' rows in the workspace), and the scaling
@@ -372,6 +375,7 @@ __global__ void __launch_bounds__(kBandThreads) band_finish_kernel(const __grid_
   const int g = blockIdx.x;
   const FaceParam P = args.dev_fp ? args.dev_fp[g] : args.fp[g];
   if (!band_level(P.m)) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the band kernel's rows of A'_L are complete
   float* __restrict__ out = args.out + (long long)g * args.out_face_stride;
   if (threadIdx.x == 0) {   // scaling coefficient: unchanged (R8)
     const int b_ = g / args.faces, f_ = g % args.faces;
@@ -417,7 +421,19 @@ hs_status launch_shift2d_band(ShiftArgs& a, int max_m, cudaStream_t st) {
   HS_SMEM_ATTR(shift2d_band_kernel, band_smem_bytes(kBandMaxLevel));
   shift2d_band_kernel<<<dim3((1u << max_m) / kBH, a.num_faces), kBandThreads, smem, st>>>(a);
   HS_CHECK_LAUNCH("shift2d_band_kernel");
-  band_finish_kernel<<<a.num_faces, kBandThreads, 0, st>>>(a);
+  {   // programmatic dependent launch: its launch overlaps the band kernel's last wave
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.num_faces);
+    cfg.blockDim = dim3(kBandThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HS_CHECK_CUDA(cudaLaunchKernelEx(&cfg, band_finish_kernel, a), "cudaLaunchKernelEx(band_finish_kernel)");
+  }
   HS_CHECK_LAUNCH("band_finish_kernel");
   return HS_OK;
 }
